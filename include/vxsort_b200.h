@@ -1,0 +1,124 @@
+/*
+ * vxsort_b200.h -- C ABI of the B200 sort (libvxsort_b200.so).
+ *
+ * Drop-in boundary for the reference's sort surface
+ *   vexsort::sort(std::span<T> keys, const SortConfig&) -> SortStats
+ *   /root/reference/proj/core/include/vexsort/vexsort.hpp:121-129
+ *   (dispatch: proj/core/src/vexsort.cpp:11-49; SortConfig vexsort.hpp:112-119;
+ *    SortStats driver.hpp:26-32; scratch_bytes vexsort.hpp:58-66).
+ * Plain pointers and sizes only.  include/vexsort_b200.hpp wraps this ABI in
+ * the reference's C++ overload set (recompile-only drop-in); INTEGRATION.md
+ * shows the binding.
+ *
+ * Errors: the reference throws std::invalid_argument (scratch too small,
+ * vexsort.cpp:23-25) and std::logic_error (config.hpp:55-59).  A C ABI cannot
+ * throw: every entry point returns a vxs_status and vxs_last_error() holds a
+ * thread-local message; the C++ wrapper rethrows.
+ *
+ * Threading: every call is reentrant per (device, stream); no global mutable
+ * state beyond per-device caches behind a mutex (reference: SPEC.md:504).
+ */
+#ifndef VXSORT_B200_H_
+#define VXSORT_B200_H_
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* The nine reference key types (vexsort.hpp:121-129) plus KV64, an alias of
+ * the K128 layout {lo = payload, hi = key} that sorts by key, then payload. */
+typedef enum {
+  VXS_I16 = 0,
+  VXS_U16 = 1,
+  VXS_I32 = 2,
+  VXS_U32 = 3,
+  VXS_F32 = 4,
+  VXS_I64 = 5,
+  VXS_U64 = 6,
+  VXS_F64 = 7,
+  VXS_K128 = 8,
+  VXS_KV64 = 9
+} vxs_key_type;
+
+/* vexsort::Order (vexsort.hpp:31) */
+typedef enum { VXS_ASCENDING = 0, VXS_DESCENDING = 1 } vxs_order;
+
+typedef enum {
+  VXS_OK = 0,
+  VXS_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  VXS_CUDA_ERROR = 2,       /* reference: none (std::runtime_error in C++) */
+  VXS_OUT_OF_MEMORY = 3,
+  VXS_INTERNAL = 4,         /* reference: std::logic_error (DASSERT) */
+  VXS_NO_DEVICE = 5
+} vxs_status;
+
+/* vexsort::SortStats (driver.hpp:26-32) first, then device extras.
+ *   max_depth         -> multiway levels executed
+ *   partition_calls   -> buckets split (multiway partitions)
+ *   base_case_calls   -> base-case items sorted (CTA-level sorts)
+ *   keys_partitioned  -> keys moved by partition passes
+ *   fallback_triggered-> more levels than the size-based estimate were needed */
+typedef struct {
+  size_t max_depth;
+  size_t partition_calls;
+  size_t base_case_calls;
+  size_t keys_partitioned;
+  int fallback_triggered;
+  int kernel_launches; /* kernels this call launched */
+  size_t workspace_bytes;
+} vxs_stats;
+
+/* Device workspace a vxs_sort call of n keys needs (CUB-style two-phase). */
+vxs_status vxs_sort_workspace_bytes(size_t n, vxs_key_type type, size_t* bytes);
+
+/* In-place sort of n keys at DEVICE pointer d_keys, stream-ordered on
+ * `stream` (a cudaStream_t; NULL = legacy default stream).  d_workspace may
+ * be NULL (then it is allocated stream-ordered).  The call synchronises the
+ * stream once (to read the device bucket scheduler's level count); if stats
+ * is non-NULL it is filled.  seed/has_seed mirror SortConfig.seed
+ * (vexsort.hpp:112-119): the output never depends on it. */
+vxs_status vxs_sort(void* d_keys, size_t n, vxs_key_type type, vxs_order order, uint64_t seed,
+                    int has_seed, void* d_workspace, size_t workspace_bytes, void* stream,
+                    vxs_stats* stats);
+
+/* The reference's host-span semantics (vexsort.cpp:11-49): h_keys is a HOST
+ * pointer; copies to the device, sorts, copies back, synchronises. */
+vxs_status vxs_sort_host(void* h_keys, size_t n, vxs_key_type type, vxs_order order, uint64_t seed,
+                         int has_seed, vxs_stats* stats);
+
+/* Distributed sample sort building blocks.
+ * vxs_sample: s stratified random samples of d_keys written to d_out as
+ *   ORDER-TRANSFORMED unsigned words of the key width (sortable as unsigned).
+ * vxs_partition: multiway partition of d_keys into nspl+1 segments by sorted
+ *   transformed-domain splitters (segment i = keys k with spl[i-1] < k <=
+ *   spl[i]); output keys (original encoding) grouped by segment in d_out,
+ *   per-segment counts (uint64) in d_seg_counts. */
+vxs_status vxs_sample(const void* d_keys, size_t n, vxs_key_type type, vxs_order order, uint64_t seed,
+                      void* d_out, int s, void* stream);
+vxs_status vxs_partition(const void* d_keys, size_t n, vxs_key_type type, vxs_order order,
+                         const void* d_splitters, int nspl, void* d_out, uint64_t* d_seg_counts,
+                         void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* Key transform as used inside the kernels (exposed for tests): encodes
+ * (inverse=0) or decodes (inverse=1) n keys in place on the device. */
+vxs_status vxs_transform(void* d_keys, size_t n, vxs_key_type type, vxs_order order, int inverse,
+                         void* stream);
+
+/* Thread-local message for the last non-OK status. */
+const char* vxs_last_error(void);
+
+/* Size in bytes of one key of this type (2, 4, 8 or 16; 0 if invalid). */
+size_t vxs_key_bytes(vxs_key_type type);
+
+/* Base-case capacity (keys per CTA sort) for this type. */
+size_t vxs_base_case_capacity(vxs_key_type type);
+
+/* Library version string. */
+const char* vxs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VXSORT_B200_H_ */

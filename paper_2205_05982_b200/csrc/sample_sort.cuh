@@ -1,0 +1,782 @@
+// sample_sort.cuh -- device kernels of the multiway (ips4o-style) sample sort.
+//
+// Reference path being replaced (/root/reference/proj/core/include/vexsort/detail):
+//   driver.hpp:123-191   Driver::recurse/sort   -> a device worklist of buckets:
+//                        each LEVEL splits every large bucket up to 256 ways
+//                        (k_sample, k_hist, k_plan, k_scatter); small buckets
+//                        go to the per-CTA base case (k_final); buckets of
+//                        equal keys are terminal (k_copy*).
+//   pivot.hpp:146-172    PivotSampler::choose_pivot -> k_sample: stratified
+//                        random 4-key chunks per bucket, sorted in smem, m
+//                        equidistant splitters (m = 2^L - 1, L <= 8).
+//   partition.hpp:197-236 Partitioner::partition (2-way, <=pivot left)
+//                        -> k_hist + k_scatter: multiway classify with a
+//                        splitter tree in smem, warp __match_any_sync/popc
+//                        ranking, block scan, smem-staged buckets, coalesced
+//                        bucket writes; each key read+written once per level.
+//   driver.hpp:142-151   degenerate recovery via scan_min_max -> equality
+//                        buckets: keys equal to a splitter land in a terminal
+//                        bucket, so all-equal / low-entropy inputs finish in
+//                        one level (no scan, no heapsort fallback).
+//   network.hpp:372-404  base case -> k_final (block_sort.cuh).
+//
+// Every bucket owns a fixed index range [start, start+size) for its whole
+// life; keys ping-pong between the caller's array A and the temp array B in
+// that range, so the final base-case/copy pass can always write into A.
+#pragma once
+#include <cstdint>
+
+#include "block_sort.cuh"
+#include "keys.cuh"
+
+namespace vxs {
+
+constexpr int kMaxL = 8;            // up to 256-way split per level
+constexpr int kChildStride = 512;   // child slots per split bucket (2*255+1 used)
+constexpr int kNumSortClasses = 5;  // base-case size classes
+constexpr int kListCopySmall = kNumSortClasses;
+constexpr int kListCopyBig = kNumSortClasses + 1;
+constexpr int kNumLists = kNumSortClasses + 2;
+constexpr int kMaxSamples = 4096;
+constexpr unsigned long long kTileMask = (1ull << 40) - 1;
+
+enum : unsigned { F_IN_B = 1u, F_RAW = 2u };
+
+struct SplitDesc {
+  unsigned long long start, size, tile_base;
+  unsigned flags, L;
+};
+
+struct Item {
+  unsigned long long start, size;
+  unsigned flags, pad;
+  unsigned long long pad2;
+};
+
+struct Ctrl {
+  unsigned long long split_packed[2];  // (count << 40) | tiles, per split list
+  unsigned long long item_count[kNumLists];
+  unsigned long long partition_calls, keys_partitioned, base_cases;
+  unsigned error, pad;
+};
+
+// Compile-time configuration per key word.
+template <typename W>
+struct Cfg {
+  // classify/scatter tile
+  static constexpr int kTileThreads = 256;
+  static constexpr int kTileItems = 16;
+  // base case capacity (largest class)
+  static constexpr int kCap = 8192;
+};
+template <>
+struct Cfg<uint32_t> {
+  static constexpr int kTileThreads = 512;
+  static constexpr int kTileItems = 16;
+  static constexpr int kCap = 8192;
+};
+template <>
+struct Cfg<uint16_t> {
+  static constexpr int kTileThreads = 512;
+  static constexpr int kTileItems = 16;
+  static constexpr int kCap = 8192;
+};
+template <>
+struct Cfg<U128> {
+  static constexpr int kTileThreads = 256;
+  static constexpr int kTileItems = 8;
+  static constexpr int kCap = 4096;
+};
+
+// Base-case classes (THREADS, ITEMS); capacity THREADS*ITEMS.
+template <int C>
+struct SortClass;
+template <>
+struct SortClass<0> {
+  static constexpr int T = 64, I = 4;
+};
+template <>
+struct SortClass<1> {
+  static constexpr int T = 128, I = 8;
+};
+template <>
+struct SortClass<2> {
+  static constexpr int T = 256, I = 8;
+};
+template <>
+struct SortClass<3> {
+  static constexpr int T = 256, I = 16;
+};
+template <>
+struct SortClass<4> {
+  static constexpr int T = 512, I = 16;
+};
+
+__host__ __device__ inline int class_for(unsigned long long size) {
+  if (size <= 256) return 0;
+  if (size <= 1024) return 1;
+  if (size <= 2048) return 2;
+  if (size <= 4096) return 3;
+  return 4;
+}
+
+template <typename W>
+struct Params {
+  W* a;  // caller's keys; final destination
+  W* b;  // temp (same length)
+  unsigned long long n;
+  int xf;          // key transform (keys.cuh)
+  int cur;         // split list read this level; children go to cur^1
+  int level;
+  int part_mode;   // 1: vxs_partition (caller splitters, output decoded into `out`)
+  unsigned long long seed;
+  Ctrl* ctrl;
+  SplitDesc* split[2];
+  W* splitters;                 // [cap_split][256]
+  unsigned long long* counts;   // [cap_split][kChildStride]
+  unsigned long long* cursors;  // [cap_split][kChildStride]
+  Item* items[kNumLists];
+  unsigned long long cap_split, cap_items;
+  W* out;                       // part_mode output
+};
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <typename W>
+__device__ __forceinline__ int ntiles_dev(unsigned long long size) {
+  constexpr int TILE = Cfg<W>::kTileThreads * Cfg<W>::kTileItems;
+  return (int)((size + TILE - 1) / TILE);
+}
+
+// Fan-out exponent for a bucket: children target ~Cap/4 keys, <= 256 ways.
+template <typename W>
+__device__ __forceinline__ int fanout_L(unsigned long long size) {
+  const unsigned long long target = Cfg<W>::kCap / 4;
+  int L = 1;
+  while (L < kMaxL && (size >> L) > target) ++L;
+  return L;
+}
+
+// ---- block helpers ---------------------------------------------------------
+// Exclusive scan of v over the block (THREADS threads, one value each);
+// returns the exclusive prefix, writes the total to *total.
+template <int THREADS, typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* total, T* scratch /*[32]*/) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) scratch[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int NW = THREADS / 32;
+    T s = lane < NW ? scratch[lane] : T(0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < NW) scratch[lane] = s;  // inclusive warp totals
+  }
+  __syncthreads();
+  const T warp_excl = warp == 0 ? T(0) : scratch[warp - 1];
+  *total = scratch[THREADS / 32 - 1];
+  const T r = warp_excl + x - v;
+  __syncthreads();
+  return r;
+}
+
+// Splitter tree in shared memory: tree[1..m] in BFS order of the implicit
+// balanced BST over the sorted splitters srt[0..m-1].
+template <typename W>
+__device__ __forceinline__ void load_tree(const W* g_srt, int L, W* tree, W* srt) {
+  const int m = (1 << L) - 1;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) srt[i] = g_srt[i];
+  __syncthreads();
+  for (int j = threadIdx.x + 1; j <= m; j += blockDim.x) {
+    const int d = 31 - __clz(j);
+    const int q = j - (1 << d);
+    const int idx = ((2 * q + 1) << (L - 1 - d)) - 1;
+    tree[j] = srt[idx];
+  }
+  __syncthreads();
+}
+
+// Child id of key x: i = #splitters < x (lower bound); an equal splitter sends
+// x to the equality bucket 2i+1, else the normal bucket 2i.  Ids ascend in key
+// order: normal_0 < eq_0 < normal_1 < ... < normal_m.
+template <typename W>
+__device__ __forceinline__ int classify(const W& x, const W* tree, const W* srt, int L) {
+  int j = 1;
+#pragma unroll
+  for (int l = 0; l < kMaxL; ++l) {
+    if (l < L) j = 2 * j + (key_lt(tree[j], x) ? 1 : 0);
+  }
+  const int i = j - (1 << L);
+  const int eq = (i < (1 << L) - 1 && key_eq(srt[i], x)) ? 1 : 0;
+  return 2 * i + eq;
+}
+
+// Find the split bucket owning global tile t (binary search on tile_base).
+__device__ __forceinline__ int find_bucket(const SplitDesc* list, int nb, unsigned long long t) {
+  int lo = 0, hi = nb - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (list[mid].tile_base <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ---- kernels ---------------------------------------------------------------
+
+// Root setup: reset counters; the whole array becomes one split bucket or one
+// base-case item (driver.hpp:172-191's n<=1 / n<=256 / recurse dispatch).
+template <typename W>
+__global__ void k_init(Params<W> P) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Ctrl* c = P.ctrl;
+  c->split_packed[0] = 0;
+  c->split_packed[1] = 0;
+  for (int i = 0; i < kNumLists; ++i) c->item_count[i] = 0;
+  c->partition_calls = c->keys_partitioned = c->base_cases = 0;
+  c->error = 0;
+  if (P.n > (unsigned long long)Cfg<W>::kCap || P.part_mode) {
+    SplitDesc d;
+    d.start = 0;
+    d.size = P.n;
+    d.tile_base = 0;
+    d.flags = F_RAW;
+    d.L = 0;
+    P.split[0][0] = d;
+    c->split_packed[0] = (1ull << 40) | (unsigned long long)ntiles_dev<W>(P.n);
+  } else if (P.n > 1) {
+    Item it;
+    it.start = 0;
+    it.size = P.n;
+    it.flags = F_RAW;
+    const int cls = class_for(P.n);
+    P.items[cls][0] = it;
+    c->item_count[cls] = 1;
+    c->base_cases = 1;
+  }
+}
+
+// Splitter selection (replaces choose_pivot, pivot.hpp:146-172): stratified
+// random 4-key chunks (cache-line friendly like the reference's 64-B chunks,
+// PAPER.md:393-398), smem bitonic sort, equidistant splitters.
+template <typename W, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  W* s = reinterpret_cast<W*>(smem_raw);
+  const unsigned long long packed = P.ctrl->split_packed[P.cur];
+  const int nb = (int)(packed >> 40);
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrl->split_packed[P.cur ^ 1] = 0;
+  SplitDesc* list = P.split[P.cur];
+  for (int p = blockIdx.x; p < nb; p += gridDim.x) {
+    SplitDesc d = list[p];
+    const int L = fanout_L<W>(d.size);
+    const int m = (1 << L) - 1;
+    int S = 16 << L;
+    if (S > kMaxSamples) S = kMaxSamples;
+    const W* src = (d.flags & F_IN_B) ? P.b : P.a;
+    const int xf = (d.flags & F_RAW) ? P.xf : XF_NONE;
+    const int nch = S / 4;
+    const unsigned long long stratum = d.size / nch;
+    for (int c = threadIdx.x; c < nch; c += THREADS) {
+      const unsigned long long lo = (unsigned long long)c * d.size / nch;
+      const unsigned long long r = mix64(P.seed ^ mix64(d.start * 0x9E3779B97F4A7C15ull + c) ^
+                                         ((unsigned long long)P.level << 56));
+      const unsigned long long span = stratum >= 4 ? stratum - 3 : 1;
+      const unsigned long long off = __umul64hi(r, span);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        unsigned long long idx = lo + off + e;
+        if (idx >= d.size) idx = d.size - 1;
+        s[4 * c + e] = enc<W>(ldg(src + d.start + idx), xf);
+      }
+    }
+    __syncthreads();
+    // bitonic sort of S (power of two) keys in smem
+    for (int size = 2; size <= S; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = threadIdx.x; i < S / 2; i += THREADS) {
+          const int lo_i = 2 * i - (i & (stride - 1));
+          const int hi_i = lo_i + stride;
+          W x = s[lo_i], y = s[hi_i];
+          const bool up = (lo_i & size) == 0;
+          if (up ? key_lt(y, x) : key_lt(x, y)) {
+            s[lo_i] = y;
+            s[hi_i] = x;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    W* g = P.splitters + (unsigned long long)p * 256;
+    const int step = S / (m + 1);
+    for (int k = threadIdx.x; k < m; k += THREADS) g[k] = s[(k + 1) * step - 1];
+    unsigned long long* cnt = P.counts + (unsigned long long)p * kChildStride;
+    for (int k = threadIdx.x; k < kChildStride; k += THREADS) cnt[k] = 0;
+    if (threadIdx.x == 0) list[p].L = (unsigned)L;
+    __syncthreads();
+  }
+}
+
+// Per-tile classification histogram (read-only pass over the level's keys).
+template <typename W>
+__global__ void __launch_bounds__(Cfg<W>::kTileThreads) k_hist(Params<W> P) {
+  constexpr int THREADS = Cfg<W>::kTileThreads;
+  constexpr int ITEMS = Cfg<W>::kTileItems;
+  constexpr int TILE = THREADS * ITEMS;
+  __shared__ W tree[256];
+  __shared__ W srt[256];
+  __shared__ unsigned hist[kChildStride];
+  __shared__ int s_p;
+  const unsigned long long packed = P.ctrl->split_packed[P.cur];
+  const int nb = (int)(packed >> 40);
+  const unsigned long long T = packed & kTileMask;
+  if (nb == 0) return;
+  const unsigned long long tpc = (T + gridDim.x - 1) / gridDim.x;
+  const unsigned long long t0 = blockIdx.x * tpc;
+  const unsigned long long t1 = t0 + tpc < T ? t0 + tpc : T;
+  if (t0 >= t1) return;
+  const SplitDesc* list = P.split[P.cur];
+  if (threadIdx.x == 0) s_p = find_bucket(list, nb, t0);
+  for (int i = threadIdx.x; i < kChildStride; i += THREADS) hist[i] = 0;
+  __syncthreads();
+  int p = s_p;
+  SplitDesc d = list[p];
+  int L = (int)d.L;
+  load_tree(P.splitters + (unsigned long long)p * 256, L, tree, srt);
+  const int lane = threadIdx.x & 31;
+  for (unsigned long long t = t0; t < t1; ++t) {
+    if (p + 1 < nb && list[p + 1].tile_base <= t) {
+      // flush and move to the next bucket
+      __syncthreads();
+      const int nc = 2 * ((1 << L) - 1) + 1;
+      for (int c = threadIdx.x; c < nc; c += THREADS) {
+        if (hist[c]) atomicAdd(P.counts + (unsigned long long)p * kChildStride + c, (unsigned long long)hist[c]);
+        hist[c] = 0;
+      }
+      while (p + 1 < nb && list[p + 1].tile_base <= t) ++p;
+      d = list[p];
+      L = (int)d.L;
+      __syncthreads();
+      load_tree(P.splitters + (unsigned long long)p * 256, L, tree, srt);
+    }
+    const W* src = (d.flags & F_IN_B) ? P.b : P.a;
+    const int xf = (d.flags & F_RAW) ? P.xf : XF_NONE;
+    const unsigned long long lo = d.start + (t - d.tile_base) * TILE;
+    const unsigned long long end = d.start + d.size;
+    const int cnt = (int)((end - lo) < (unsigned long long)TILE ? (end - lo) : TILE);
+    W k[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * THREADS + threadIdx.x;
+      k[i] = idx < cnt ? enc<W>(ldcs(src + lo + idx), xf) : key_max<W>();
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * THREADS + threadIdx.x;
+      const bool valid = idx < cnt;
+      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+      if (valid) {
+        const int b = classify(k[i], tree, srt, L);
+        const unsigned peers = __match_any_sync(vmask, b);
+        if (lane == __ffs(peers) - 1) atomicAdd(&hist[b], (unsigned)__popc(peers));
+      }
+    }
+  }
+  __syncthreads();
+  const int nc = 2 * ((1 << L) - 1) + 1;
+  for (int c = threadIdx.x; c < nc; c += THREADS) {
+    if (hist[c]) atomicAdd(P.counts + (unsigned long long)p * kChildStride + c, (unsigned long long)hist[c]);
+  }
+}
+
+// Per split bucket: child offsets -> cursors; children become next-level
+// split buckets, base-case items (grouping adjacent small children into one
+// item of <= Cap keys) or copy items (equality buckets).
+template <typename W>
+__global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
+  constexpr int THREADS = kChildStride;
+  constexpr unsigned long long CAP = Cfg<W>::kCap;
+  __shared__ unsigned long long s_cnt[kChildStride];
+  __shared__ unsigned long long s_off[kChildStride];
+  __shared__ unsigned long long scan_scratch[32];
+  // grouped items built by thread 0
+  __shared__ unsigned long long g_start[kChildStride + 8];
+  __shared__ unsigned long long g_size[kChildStride + 8];
+  __shared__ int g_list[kChildStride + 8];
+  __shared__ int s_ng;
+  __shared__ unsigned long long s_res[kNumLists];
+  __shared__ unsigned long long s_split_base;
+  const unsigned long long packed = P.ctrl->split_packed[P.cur];
+  const int nb = (int)(packed >> 40);
+  const SplitDesc* list = P.split[P.cur];
+  const int nxt = P.cur ^ 1;
+  for (int p = blockIdx.x; p < nb; p += gridDim.x) {
+    const SplitDesc d = list[p];
+    const int L = (int)d.L;
+    const int nc = 2 * ((1 << L) - 1) + 1;
+    const int c = threadIdx.x;
+    const unsigned long long cnt = c < nc ? P.counts[(unsigned long long)p * kChildStride + c] : 0;
+    unsigned long long total;
+    const unsigned long long off = block_exclusive_scan<THREADS>(cnt, &total, scan_scratch);
+    if (c < nc) P.cursors[(unsigned long long)p * kChildStride + c] = d.start + off;
+    s_cnt[c] = cnt;
+    s_off[c] = off;
+    const unsigned child_flags = (d.flags & F_IN_B) ? 0u : F_IN_B;  // raw cleared
+    if (P.part_mode) {
+      __syncthreads();
+      continue;
+    }
+    // next-level split children
+    const bool is_split = c < nc && (c & 1) == 0 && cnt > CAP;
+    const unsigned long long my_tiles = is_split ? (unsigned long long)ntiles_dev<W>(cnt) : 0ull;
+    const unsigned long long pk = is_split ? ((1ull << 40) | my_tiles) : 0ull;
+    unsigned long long pk_total;
+    const unsigned long long pk_excl = block_exclusive_scan<THREADS>(pk, &pk_total, scan_scratch);
+    if (c == 0 && pk_total) s_split_base = atomicAdd(&P.ctrl->split_packed[nxt], pk_total);
+    __syncthreads();
+    if (is_split) {
+      const unsigned long long base = s_split_base + pk_excl;
+      const unsigned long long q = base >> 40;
+      if (q < P.cap_split) {
+        SplitDesc nd;
+        nd.start = d.start + off;
+        nd.size = cnt;
+        nd.tile_base = base & kTileMask;
+        nd.flags = child_flags;
+        nd.L = 0;
+        P.split[nxt][q] = nd;
+      } else {
+        P.ctrl->error = 1;
+      }
+    }
+    // group the remaining children (sequential, smem only)
+    if (c == 0) {
+      int ng = 0;
+      unsigned long long gs = 0, gz = 0;
+      bool gsort = false;
+      const bool need_copy = (child_flags & F_IN_B) || P.xf != XF_NONE;
+      auto emit = [&]() {
+        if (gz == 0) return;
+        int lst;
+        if (gsort) lst = class_for(gz);
+        else lst = need_copy ? kListCopySmall : -1;
+        if (lst >= 0) {
+          g_start[ng] = gs;
+          g_size[ng] = gz;
+          g_list[ng] = lst;
+          ++ng;
+        }
+        gz = 0;
+        gsort = false;
+      };
+      for (int ch = 0; ch < nc; ++ch) {
+        const unsigned long long s = s_cnt[ch];
+        if (s == 0) continue;
+        const bool eq = (ch & 1) != 0;
+        if (!eq && s > CAP) {  // split child
+          emit();
+          continue;
+        }
+        if (eq && s > CAP) {  // big equality bucket: one cooperative copy item
+          emit();
+          if (need_copy) {
+            g_start[ng] = d.start + s_off[ch];
+            g_size[ng] = s;
+            g_list[ng] = kListCopyBig;
+            ++ng;
+          }
+          continue;
+        }
+        if (gz + s > CAP) emit();
+        if (gz == 0) gs = d.start + s_off[ch];
+        gz += s;
+        gsort = gsort || (!eq && s > 1);
+      }
+      emit();
+      s_ng = ng;
+      for (int l = 0; l < kNumLists; ++l) s_res[l] = 0;
+      for (int g = 0; g < ng; ++g) s_res[g_list[g]] += 1;
+      unsigned long long nsort = 0;
+      for (int l = 0; l < kNumLists; ++l) {
+        const unsigned long long k = s_res[l];
+        if (l < kNumSortClasses) nsort += k;
+        s_res[l] = k ? atomicAdd(&P.ctrl->item_count[l], k) : 0;
+      }
+      atomicAdd(&P.ctrl->partition_calls, 1ull);
+      atomicAdd(&P.ctrl->keys_partitioned, d.size);
+      if (nsort) atomicAdd(&P.ctrl->base_cases, nsort);
+    }
+    __syncthreads();
+    if (c < 32) {
+      // write items: warp 0, in order per list (rank among same-list items)
+      const int ng = s_ng;
+      for (int g0 = 0; g0 < ng; g0 += 32) {
+        const int g = g0 + c;
+        int lst = g < ng ? g_list[g] : -1;
+        // rank of this group among earlier groups of the same list
+        unsigned long long rank = 0;
+        for (int h = 0; h < g0; ++h) rank += (g_list[h] == lst);
+        const unsigned same = __match_any_sync(0xffffffffu, lst);
+        rank += __popc(same & lanemask_lt());
+        if (g < ng) {
+          const unsigned long long slot = s_res[lst] + rank;
+          if (slot < P.cap_items) {
+            Item it;
+            it.start = g_start[g];
+            it.size = g_size[g];
+            it.flags = child_flags;
+            it.pad = 0;
+            it.pad2 = 0;
+            P.items[lst][slot] = it;
+          } else {
+            P.ctrl->error = 2;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Scatter: classify again, rank within the tile per child with warp-aggregated
+// smem atomics (__match_any_sync + popc), block scan, stage the tile in smem
+// grouped by child, reserve each child's global range with one atomic per
+// (tile, child), then write each child run with consecutive threads.
+template <typename W>
+__global__ void __launch_bounds__(Cfg<W>::kTileThreads) k_scatter(Params<W> P) {
+  constexpr int THREADS = Cfg<W>::kTileThreads;
+  constexpr int ITEMS = Cfg<W>::kTileItems;
+  constexpr int TILE = THREADS * ITEMS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  W* stage = reinterpret_cast<W*>(smem_raw);
+  unsigned short* stage_b = reinterpret_cast<unsigned short*>(stage + TILE);
+  __shared__ W tree[256];
+  __shared__ W srt[256];
+  __shared__ unsigned hist[kChildStride];
+  __shared__ unsigned toff[kChildStride];
+  __shared__ unsigned long long gbase[kChildStride];
+  __shared__ unsigned scan_scratch[32];
+  __shared__ int s_p;
+  const unsigned long long packed = P.ctrl->split_packed[P.cur];
+  const int nb = (int)(packed >> 40);
+  const unsigned long long T = packed & kTileMask;
+  if (nb == 0) return;
+  const unsigned long long tpc = (T + gridDim.x - 1) / gridDim.x;
+  const unsigned long long t0 = blockIdx.x * tpc;
+  const unsigned long long t1 = t0 + tpc < T ? t0 + tpc : T;
+  if (t0 >= t1) return;
+  const SplitDesc* list = P.split[P.cur];
+  if (threadIdx.x == 0) s_p = find_bucket(list, nb, t0);
+  __syncthreads();
+  int p = s_p;
+  SplitDesc d = list[p];
+  int L = (int)d.L;
+  load_tree(P.splitters + (unsigned long long)p * 256, L, tree, srt);
+  const int lane = threadIdx.x & 31;
+  W* dst_buf = P.part_mode ? P.out : ((d.flags & F_IN_B) ? P.a : P.b);
+  const int out_xf = P.part_mode ? P.xf : XF_NONE;
+  for (unsigned long long t = t0; t < t1; ++t) {
+    if (p + 1 < nb && list[p + 1].tile_base <= t) {
+      while (p + 1 < nb && list[p + 1].tile_base <= t) ++p;
+      d = list[p];
+      L = (int)d.L;
+      dst_buf = P.part_mode ? P.out : ((d.flags & F_IN_B) ? P.a : P.b);
+      load_tree(P.splitters + (unsigned long long)p * 256, L, tree, srt);
+    }
+    const int nc = 2 * ((1 << L) - 1) + 1;
+    for (int i = threadIdx.x; i < kChildStride; i += THREADS) hist[i] = 0;
+    const W* src = (d.flags & F_IN_B) ? P.b : P.a;
+    const int xf = (d.flags & F_RAW) ? P.xf : XF_NONE;
+    const unsigned long long lo = d.start + (t - d.tile_base) * TILE;
+    const unsigned long long end = d.start + d.size;
+    const int cnt = (int)((end - lo) < (unsigned long long)TILE ? (end - lo) : TILE);
+    W k[ITEMS];
+    int bk[ITEMS];
+    unsigned rk[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * THREADS + threadIdx.x;
+      k[i] = idx < cnt ? enc<W>(ldcs(src + lo + idx), xf) : key_max<W>();
+    }
+    __syncthreads();  // hist zeroed
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * THREADS + threadIdx.x;
+      const bool valid = idx < cnt;
+      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+      bk[i] = -1;
+      rk[i] = 0;
+      if (valid) {
+        const int b = classify(k[i], tree, srt, L);
+        const unsigned peers = __match_any_sync(vmask, b);
+        const int leader = __ffs(peers) - 1;
+        unsigned base = 0;
+        if (lane == leader) base = atomicAdd(&hist[b], (unsigned)__popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        bk[i] = b;
+        rk[i] = base + __popc(peers & lanemask_lt());
+      }
+    }
+    __syncthreads();
+    // exclusive scan of the tile histogram (THREADS >= 256 -> 2 per thread max)
+    {
+      constexpr int PER = kChildStride / THREADS > 0 ? kChildStride / THREADS : 1;
+      unsigned v[PER];
+      unsigned sum = 0;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int c = threadIdx.x * PER + j;
+        v[j] = c < kChildStride ? hist[c] : 0;
+        sum += v[j];
+      }
+      unsigned tot;
+      unsigned ex = block_exclusive_scan<THREADS>(sum, &tot, scan_scratch);
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int c = threadIdx.x * PER + j;
+        if (c < kChildStride) {
+          toff[c] = ex;
+          if (v[j] && c < nc)
+            gbase[c] = atomicAdd(P.cursors + (unsigned long long)p * kChildStride + c, (unsigned long long)v[j]);
+        }
+        ex += v[j];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      if (bk[i] >= 0) {
+        const unsigned pos = toff[bk[i]] + rk[i];
+        stage[pos] = k[i];
+        stage_b[pos] = (unsigned short)bk[i];
+      }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < cnt; j += THREADS) {
+      const int c = stage_b[j];
+      const unsigned long long dst = gbase[c] + (unsigned long long)(j - (int)toff[c]);
+      dst_buf[dst] = dec<W>(stage[j], out_xf);
+    }
+    __syncthreads();
+  }
+}
+
+// Base case over one size class: load <= T*I keys, pad with the transformed
+// maximum, block_sort, decode, write back into A.
+template <typename W, int CLS>
+__global__ void __launch_bounds__(SortClass<CLS>::T) k_final(Params<W> P) {
+  constexpr int THREADS = SortClass<CLS>::T;
+  constexpr int ITEMS = SortClass<CLS>::I;
+  constexpr int TOTAL = THREADS * ITEMS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  W* sm = reinterpret_cast<W*>(smem_raw);
+  const unsigned long long nitems = P.ctrl->item_count[CLS];
+  const Item* items = P.items[CLS];
+  for (unsigned long long it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const Item item = items[it];
+    const W* src = (item.flags & F_IN_B) ? P.b : P.a;
+    const int xf = (item.flags & F_RAW) ? P.xf : XF_NONE;
+    const int size = (int)item.size;
+    W k[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * THREADS + threadIdx.x;
+      k[i] = idx < size ? enc<W>(ldcs(src + item.start + idx), xf) : key_max<W>();
+    }
+    block_sort<W, THREADS, ITEMS>(k, sm);
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) sm[threadIdx.x * ITEMS + i] = k[i];
+    __syncthreads();
+    W* dst = P.a + item.start;
+    for (int idx = threadIdx.x; idx < size; idx += THREADS) dst[idx] = dec<W>(sm[idx], P.xf);
+    __syncthreads();
+  }
+  (void)TOTAL;
+}
+
+// Copy (decode) sorted runs that need no sorting: equality buckets and groups
+// of single keys, B -> A or decode-in-place in A.
+template <typename W>
+__global__ void __launch_bounds__(256) k_copy(Params<W> P) {
+  // small items: one CTA per item
+  {
+    const unsigned long long nitems = P.ctrl->item_count[kListCopySmall];
+    const Item* items = P.items[kListCopySmall];
+    for (unsigned long long it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const Item item = items[it];
+      const W* src = ((item.flags & F_IN_B) ? P.b : P.a) + item.start;
+      W* dst = P.a + item.start;
+      for (unsigned long long i = threadIdx.x; i < item.size; i += 256) dst[i] = dec<W>(ldcs(src + i), P.xf);
+    }
+  }
+  // big items: every CTA takes strided chunks of every item
+  {
+    const unsigned long long nitems = P.ctrl->item_count[kListCopyBig];
+    const Item* items = P.items[kListCopyBig];
+    constexpr unsigned long long CH = 4096;
+    for (unsigned long long it = 0; it < nitems; ++it) {
+      const Item item = items[it];
+      const W* src = ((item.flags & F_IN_B) ? P.b : P.a) + item.start;
+      W* dst = P.a + item.start;
+      const unsigned long long nch = (item.size + CH - 1) / CH;
+      for (unsigned long long ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+        const unsigned long long e = (ch + 1) * CH < item.size ? (ch + 1) * CH : item.size;
+        for (unsigned long long i = ch * CH + threadIdx.x; i < e; i += 256) dst[i] = dec<W>(ldcs(src + i), P.xf);
+      }
+    }
+  }
+}
+
+// Sampling for the distributed sort: s keys (transformed domain), stratified.
+template <typename W>
+__global__ void k_sample_out(const W* keys, unsigned long long n, int xf, unsigned long long seed, W* out,
+                             int s) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < s; c += gridDim.x * blockDim.x) {
+    const unsigned long long lo = (unsigned long long)c * n / s;
+    const unsigned long long hi = (unsigned long long)(c + 1) * n / s;
+    const unsigned long long span = hi > lo ? hi - lo : 1;
+    const unsigned long long r = mix64(seed ^ mix64(0xA5A5ull + c));
+    unsigned long long idx = lo + __umul64hi(r, span);
+    if (idx >= n) idx = n - 1;
+    out[c] = enc<W>(ldg(keys + idx), xf);
+  }
+}
+
+// Distributed partition: install the caller's splitters (transformed domain,
+// sorted, nspl of them) as the root bucket's tree, padded with the maximum.
+template <typename W>
+__global__ void k_part_setup(Params<W> P, const W* spl, int nspl, int L) {
+  const int m = (1 << L) - 1;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) P.splitters[i] = i < nspl ? spl[i] : key_max<W>();
+  for (int i = threadIdx.x; i < kChildStride; i += blockDim.x) P.counts[i] = 0;
+  if (threadIdx.x == 0) P.split[0][0].L = (unsigned)L;
+}
+
+// Per-segment counts: segment i holds children 2i (keys between splitters)
+// and 2i+1 (keys equal to splitter i).
+template <typename W>
+__global__ void k_part_counts(Params<W> P, int nseg, unsigned long long* seg_counts) {
+  for (int i = threadIdx.x; i < nseg; i += blockDim.x) seg_counts[i] = P.counts[2 * i] + P.counts[2 * i + 1];
+}
+
+}  // namespace vxs

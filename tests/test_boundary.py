@@ -1,0 +1,81 @@
+"""The drop-in boundary, checked without a GPU: the C-ABI library loads and
+exports every symbol include/*.h declares; the Python mirror of the reference
+API validates arguments like the reference (vexsort.cpp:19-31)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2205_05982_b200 as vx
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    syms = set()
+    inc = os.path.join(ROOT, "include")
+    for f in os.listdir(inc):
+        if f.endswith(".h"):
+            src = open(os.path.join(inc, f)).read()
+            syms |= set(re.findall(r"\b(vxs_[a-z_0-9]+)\s*\(", src))
+    return syms
+
+
+def test_library_exports_every_declared_symbol():
+    lib = vx.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 10
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(vx.EXPORTED_SYMBOLS) == syms
+
+
+def test_library_is_sm100a():
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {vx.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+
+
+def test_host_only_queries():
+    assert vx.lib().vxs_version().startswith(b"vxsort_b200")
+    for kt, b in vx.KEY_BYTES.items():
+        assert vx.lib().vxs_key_bytes(vx.KEY_CODE[kt]) == b
+    assert vx.base_case_capacity("u64") >= 4096
+    ws = vx.workspace_bytes(100_000_000, "u64")
+    assert 800_000_000 <= ws < 1_200_000_000  # temp keys + O(n/cap) scheduler state
+    assert vx.workspace_bytes(0, "u32") > 0
+
+
+def test_invalid_arguments_map_to_value_error():
+    lib = vx.lib()
+    st = vx.SortStats()
+    # unknown key type / order -> VXS_INVALID_ARGUMENT without touching a GPU
+    assert lib.vxs_sort(None, 0, 42, 0, 0, 0, None, 0, None, ctypes.byref(st)) == 1
+    assert lib.vxs_sort(None, 0, 3, 7, 0, 0, None, 0, None, ctypes.byref(st)) == 1
+    assert lib.vxs_sort(None, 5, 3, 0, 0, 0, None, 0, None, ctypes.byref(st)) == 1
+    assert b"NULL" in lib.vxs_last_error()
+    with pytest.raises(ValueError):
+        vx.sort(np.zeros(4, np.uint64), vx.SortConfig(scratch=vx.SortScratch(16)))
+    with pytest.raises(ValueError):
+        vx.sort(np.zeros((4, 2), np.uint64))  # K128 needs an explicit key type
+    with pytest.raises(ValueError):
+        vx.sort(np.zeros(4, np.complex64))
+
+
+def test_trivial_host_sorts_need_no_device():
+    # n <= 1 returns before touching the device (driver.hpp:175)
+    for n in (0, 1):
+        x = np.arange(n, dtype=np.uint32)
+        st = vx.sort(x)
+        assert st.max_depth == 0 and st.partition_calls == 0
+
+
+def test_cpp_header_mirrors_reference_surface():
+    hpp = open(os.path.join(ROOT, "include", "vexsort_b200.hpp")).read()
+    for t in ("std::int16_t", "std::uint16_t", "std::int32_t", "std::uint32_t", "float",
+              "std::int64_t", "std::uint64_t", "double", "K128"):
+        assert re.search(r"SortStats sort\(std::span<%s> keys" % re.escape(t), hpp), t
+    for name in ("struct SortConfig", "class SortScratch", "scratch_bytes", "enum class Order",
+                 "enum class Backend", "wide_backend_is_simd"):
+        assert name in hpp
