@@ -57,7 +57,7 @@ int grid_for(const void* fn, int threads, size_t smem) {
   auto it = di.occ.find(fn);
   int occ;
   if (it == di.occ.end()) {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem > 0) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
     if (occ < 1) occ = 1;
