@@ -106,6 +106,19 @@ vxs_status vxs_partition(const void* d_keys, size_t n, vxs_key_type type, vxs_or
 vxs_status vxs_transform(void* d_keys, size_t n, vxs_key_type type, vxs_order order, int inverse,
                          void* stream);
 
+/* Measurement hooks (bench.py): when enabled, every kernel the library
+ * launches is bracketed by CUDA events on its launching stream; read()
+ * resolves them (synchronising) into per-kernel launch counts and device
+ * milliseconds.  Off by default; costs two event records per launch. */
+typedef struct {
+  char name[32];
+  long long launches;
+  double total_ms;
+} vxs_kernel_profile;
+vxs_status vxs_profile_enable(int on);
+void vxs_profile_reset(void);
+int vxs_profile_read(vxs_kernel_profile* out, int cap);
+
 /* Thread-local message for the last non-OK status. */
 const char* vxs_last_error(void);
 

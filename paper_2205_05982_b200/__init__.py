@@ -131,6 +131,9 @@ def lib():
         L.vxs_key_bytes.restype = sz
         L.vxs_base_case_capacity.argtypes = [i]
         L.vxs_base_case_capacity.restype = sz
+        L.vxs_profile_enable.argtypes = [i]
+        L.vxs_profile_read.argtypes = [ctypes.c_void_p, i]
+        L.vxs_profile_read.restype = i
         for fn in ("vxs_sort", "vxs_sort_host", "vxs_sort_workspace_bytes", "vxs_sample",
                    "vxs_partition", "vxs_transform"):
             getattr(L, fn).restype = ctypes.c_int
@@ -140,7 +143,27 @@ def lib():
 
 EXPORTED_SYMBOLS = ["vxs_sort_workspace_bytes", "vxs_sort", "vxs_sort_host", "vxs_sample",
                     "vxs_partition", "vxs_transform", "vxs_last_error", "vxs_key_bytes",
-                    "vxs_base_case_capacity", "vxs_version"]
+                    "vxs_base_case_capacity", "vxs_version", "vxs_profile_enable",
+                    "vxs_profile_reset", "vxs_profile_read"]
+
+
+class KernelProfile(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_longlong), ("total_ms", ctypes.c_double)]
+
+
+def profile_enable(on: bool = True):
+    lib().vxs_profile_enable(int(bool(on)))
+
+
+def profile_reset():
+    lib().vxs_profile_reset()
+
+
+def profile_read():
+    """{kernel name: (launches, total device ms)} since the last reset."""
+    arr = (KernelProfile * 32)()
+    k = lib().vxs_profile_read(arr, 32)
+    return {arr[i].name.decode(): (int(arr[i].launches), float(arr[i].total_ms)) for i in range(k)}
 
 
 def _check(rc: int):

@@ -13,6 +13,7 @@
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
+#include <vector>
 
 #include "../../include/vxsort_b200.h"
 #include "sample_sort.cuh"
@@ -39,6 +40,55 @@ vxs_status cuda_fail(cudaError_t e, const char* where) {
   } while (0)
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ---- optional per-kernel event timing (measurement tools only) -----------
+enum KernelId : int {
+  K_INIT = 0, K_SAMPLE, K_HIST, K_PLAN, K_SCATTER, K_FINAL0, K_FINAL1, K_FINAL2, K_FINAL3, K_FINAL4,
+  K_COPY, K_PART, K_MISC, K_COUNT
+};
+const char* kKernelNames[K_COUNT] = {"k_init", "k_sample", "k_hist", "k_plan", "k_scatter", "k_final_c0",
+                                     "k_final_c1", "k_final_c2", "k_final_c3", "k_final_c4", "k_copy",
+                                     "k_part", "k_misc"};
+struct Prof {
+  bool on = false;
+  std::mutex mu;
+  struct Rec { int id; cudaEvent_t a, b; };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms[K_COUNT] = {};
+  long long launches[K_COUNT] = {};
+} g_prof;
+
+cudaEvent_t prof_event() {
+  if (!g_prof.pool.empty()) {
+    cudaEvent_t e = g_prof.pool.back();
+    g_prof.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// RAII bracket around one launch on stream st.
+struct ProfScope {
+  int id;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(int id_, cudaStream_t st_) : id(id_), st(st_) {
+    if (!g_prof.on) return;
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    a = prof_event();
+    cudaEventRecord(a, st);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    cudaEvent_t b = prof_event();
+    cudaEventRecord(b, st);
+    g_prof.pending.push_back({id, a, b});
+  }
+};
 
 // ---- per-device caches (behind a mutex) -----------------------------------
 struct DevInfo {
@@ -146,21 +196,25 @@ template <typename W>
 vxs_status launch_level(Params<W>& P, cudaStream_t st, int& launches) {
   constexpr int kSampleThreads = 512;
   {
+    ProfScope ps(K_SAMPLE, st);
     auto fn = k_sample<W, kSampleThreads>;
     const int g = grid_for((const void*)fn, kSampleThreads, sample_smem<W>());
     fn<<<g, kSampleThreads, sample_smem<W>(), st>>>(P);
   }
   {
+    ProfScope ps(K_HIST, st);
     auto fn = k_hist<W>;
     const int g = grid_for((const void*)fn, Cfg<W>::kTileThreads, 0);
     fn<<<g, Cfg<W>::kTileThreads, 0, st>>>(P);
   }
   {
+    ProfScope ps(K_PLAN, st);
     auto fn = k_plan<W>;
     const int g = grid_for((const void*)fn, kChildStride, 0);
     fn<<<g, kChildStride, 0, st>>>(P);
   }
   {
+    ProfScope ps(K_SCATTER, st);
     auto fn = k_scatter<W>;
     const int g = grid_for((const void*)fn, Cfg<W>::kTileThreads, scatter_smem<W>());
     fn<<<g, Cfg<W>::kTileThreads, scatter_smem<W>(), st>>>(P);
@@ -174,6 +228,7 @@ template <typename W, int CLS>
 void launch_final(Params<W>& P, unsigned long long count, cudaStream_t st) {
   constexpr int T = SortClass<CLS>::T;
   constexpr size_t smem = (size_t)T * SortClass<CLS>::I * sizeof(W);
+  ProfScope ps(K_FINAL0 + CLS, st);
   auto fn = k_final<W, CLS>;
   int g = grid_for((const void*)fn, T, smem);
   if ((unsigned long long)g > count) g = (int)count;
@@ -198,7 +253,10 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
   }
   Params<W> P = make_params<W>(keys, n, xf, seed, static_cast<unsigned char*>(ws), L);
   int launches = 0;
-  k_init<W><<<1, 32, 0, st>>>(P);
+  {
+    ProfScope ps(K_INIT, st);
+    k_init<W><<<1, 32, 0, st>>>(P);
+  }
   ++launches;
   Ctrl h{};
   int levels = 0;
@@ -240,6 +298,7 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
     if (h.item_count[4]) { launch_final<W, 4>(P, h.item_count[4], st); ++launches; }
   }
   if (h.item_count[kListCopySmall] || h.item_count[kListCopyBig]) {
+    ProfScope ps(K_COPY, st);
     auto fn = k_copy<W>;
     const int g = grid_for((const void*)fn, 256, 0);
     fn<<<g, 256, 0, st>>>(P);
@@ -314,6 +373,49 @@ __global__ void k_xform(W* keys, unsigned long long n, int xf, int inverse) {
 using namespace vxs;
 
 extern "C" {
+
+vxs_status vxs_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  g_prof.on = on != 0;
+  return VXS_OK;
+}
+
+void vxs_profile_reset(void) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  for (auto& r : g_prof.pending) {
+    cudaEventSynchronize(r.b);
+    g_prof.pool.push_back(r.a);
+    g_prof.pool.push_back(r.b);
+  }
+  g_prof.pending.clear();
+  for (int i = 0; i < K_COUNT; ++i) {
+    g_prof.ms[i] = 0;
+    g_prof.launches[i] = 0;
+  }
+}
+
+int vxs_profile_read(vxs_kernel_profile* out, int cap) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  for (auto& r : g_prof.pending) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    g_prof.ms[r.id] += ms;
+    g_prof.launches[r.id] += 1;
+    g_prof.pool.push_back(r.a);
+    g_prof.pool.push_back(r.b);
+  }
+  g_prof.pending.clear();
+  int k = 0;
+  for (int i = 0; i < K_COUNT && k < cap; ++i) {
+    if (!g_prof.launches[i]) continue;
+    std::snprintf(out[k].name, sizeof(out[k].name), "%s", kKernelNames[i]);
+    out[k].launches = g_prof.launches[i];
+    out[k].total_ms = g_prof.ms[i];
+    ++k;
+  }
+  return k;
+}
 
 const char* vxs_version(void) { return "vxsort_b200 0.1 (sm_100a)"; }
 
