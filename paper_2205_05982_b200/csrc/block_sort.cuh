@@ -82,15 +82,27 @@ __device__ __forceinline__ void warp_bitonic_merge(W (&k)[N], int lane) {
   }
 }
 
-// Merge-path partition: number of elements taken from A among the first
-// `diag` outputs of merge(A[0..la), B[0..lb)), ties taken from A.
+// Shared-memory index padding: one spare slot per 128 bytes, so blocked
+// accesses (lane stride ITEMS) and merge-path windows hit distinct banks.
 template <typename W>
-__device__ __forceinline__ int merge_path(const W* A, int la, const W* B, int lb, int diag) {
+__host__ __device__ constexpr int pad_idx(int i) {
+  return i + i / (128 / (int)sizeof(W));
+}
+template <typename W>
+__host__ __device__ constexpr int padded_size(int n) {
+  return n + n / (128 / (int)sizeof(W)) + 1;
+}
+
+// Merge-path partition: number of elements taken from A among the first
+// `diag` outputs of merge(A[0..la), B[0..lb)), ties taken from A.  A and B
+// are offsets into the padded smem array S.
+template <typename W>
+__device__ __forceinline__ int merge_path(const W* S, int a0, int la, int b0, int lb, int diag) {
   int lo = diag > lb ? diag - lb : 0;
   int hi = diag < la ? diag : la;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (!key_lt(B[diag - 1 - mid], A[mid])) lo = mid + 1;
+    if (!key_lt(S[pad_idx<W>(b0 + diag - 1 - mid)], S[pad_idx<W>(a0 + mid)])) lo = mid + 1;
     else hi = mid;
   }
   return lo;
@@ -98,43 +110,51 @@ __device__ __forceinline__ int merge_path(const W* A, int la, const W* B, int lb
 
 // Sort THREADS*ITEMS keys.  On entry k[] holds this thread's keys (any
 // arrangement); on exit k[] holds keys blocked and sorted: thread t owns
-// sorted positions [t*ITEMS, (t+1)*ITEMS).  `smem` must hold THREADS*ITEMS W.
-template <typename W, int THREADS, int ITEMS>
+// sorted positions [t*ITEMS, (t+1)*ITEMS).  `smem` must hold
+// padded_size<W>(THREADS*ITEMS) W; element i lives at smem[pad_idx<W>(i)].
+// WARP_NET: merge the first 5 levels (runs up to 32*ITEMS) with the
+// __shfl_xor_sync bitonic network instead of shared-memory merge path (used
+// for the smallest class, where one or two warps hold the whole bucket).
+template <typename W, int THREADS, int ITEMS, bool WARP_NET = false>
 __device__ __forceinline__ void block_sort(W (&k)[ITEMS], W* smem) {
   const int tid = threadIdx.x;
-  const int lane = tid & 31;
   thread_sort<W, ITEMS>(k);
-  // Warp level via shuffles: runs of 32*ITEMS keys.
-  warp_bitonic_merge<W, ITEMS>(k, lane);
-  constexpr int WARP_RUN = 32 * ITEMS;
+  int first_run = ITEMS;
+  if constexpr (WARP_NET) {
+    warp_bitonic_merge<W, ITEMS>(k, tid & 31);
+    first_run = 32 * ITEMS;
+  }
   constexpr int TOTAL = THREADS * ITEMS;
 #pragma unroll 1
-  for (int run = WARP_RUN; run < TOTAL; run <<= 1) {
+  for (int run = first_run; run < TOTAL; run <<= 1) {
     // stage blocked
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) smem[tid * ITEMS + i] = k[i];
+    for (int i = 0; i < ITEMS; ++i) smem[pad_idx<W>(tid * ITEMS + i)] = k[i];
     __syncthreads();
     const int group_threads = (2 * run) / ITEMS;
     const int g = tid / group_threads;
     const int r = tid - g * group_threads;
-    const W* A = smem + g * 2 * run;
-    const W* B = A + run;
+    const int a0 = g * 2 * run;
+    const int b0 = a0 + run;
     const int diag = r * ITEMS;
-    const int a = merge_path(A, run, B, run, diag);
+    const int a = merge_path(smem, a0, run, b0, run, diag);
+    // Branch-free serial merge: one smem load per output refills the side
+    // just consumed; exhausted sides read as the maximum key.
     int ai = a, bi = diag - a;
-    W va = ai < run ? A[ai] : key_max<W>();
-    W vb = bi < run ? B[bi] : key_max<W>();
+    W va = ai < run ? smem[pad_idx<W>(a0 + ai)] : key_max<W>();
+    W vb = bi < run ? smem[pad_idx<W>(b0 + bi)] : key_max<W>();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const bool take_a = (bi >= run) || (ai < run && !key_lt(vb, va));
-      if (take_a) {
-        k[i] = va;
-        ++ai;
-        va = ai < run ? A[ai] : key_max<W>();
-      } else {
-        k[i] = vb;
-        ++bi;
-        vb = bi < run ? B[bi] : key_max<W>();
+      k[i] = take_a ? va : vb;
+      ai += take_a ? 1 : 0;
+      bi += take_a ? 0 : 1;
+      if (i + 1 < ITEMS) {
+        const int nidx = take_a ? ai : bi;
+        const int base = take_a ? a0 : b0;
+        const W nv = nidx < run ? smem[pad_idx<W>(base + nidx)] : key_max<W>();
+        va = take_a ? nv : va;
+        vb = take_a ? vb : nv;
       }
     }
     __syncthreads();

@@ -83,6 +83,87 @@ __host__ __device__ __forceinline__ unsigned long long key_max<unsigned long lon
 template <>
 __host__ __device__ __forceinline__ U128 key_max<U128>() { return U128{~0ull, ~0ull}; }
 
+// ---- arithmetic used by the splitter lookup table --------------------------
+__host__ __device__ __forceinline__ uint16_t key_sub(uint16_t a, uint16_t b) { return uint16_t(a - b); }
+__host__ __device__ __forceinline__ uint32_t key_sub(uint32_t a, uint32_t b) { return a - b; }
+__host__ __device__ __forceinline__ unsigned long long key_sub(unsigned long long a, unsigned long long b) {
+  return a - b;
+}
+__host__ __device__ __forceinline__ U128 key_sub(const U128& a, const U128& b) {
+  const unsigned long long lo = a.lo - b.lo;
+  return U128{lo, a.hi - b.hi - (a.lo < b.lo ? 1ull : 0ull)};
+}
+// Low 32 bits of (d >> s); s may exceed the word width (returns 0).
+__device__ __forceinline__ unsigned key_shr32(uint16_t d, int s) { return s >= 16 ? 0u : (unsigned)(d >> s); }
+__device__ __forceinline__ unsigned key_shr32(uint32_t d, int s) { return s >= 32 ? 0u : (d >> s); }
+__device__ __forceinline__ unsigned key_shr32(unsigned long long d, int s) {
+  return s >= 64 ? 0u : (unsigned)(d >> s);
+}
+__device__ __forceinline__ unsigned key_shr32(const U128& d, int s) {
+  if (s >= 128) return 0u;
+  if (s >= 64) return (unsigned)(d.hi >> (s - 64));
+  if (s == 0) return (unsigned)d.lo;
+  return (unsigned)((d.lo >> s) | (d.hi << (64 - s)));
+}
+// Number of significant bits.
+__device__ __forceinline__ int key_bitlen(uint16_t d) { return 32 - __clz((unsigned)d); }
+__device__ __forceinline__ int key_bitlen(uint32_t d) { return 32 - __clz(d); }
+__device__ __forceinline__ int key_bitlen(unsigned long long d) { return 64 - __clzll(d); }
+__device__ __forceinline__ int key_bitlen(const U128& d) {
+  return d.hi ? 128 - __clzll(d.hi) : 64 - __clzll(d.lo);
+}
+// lo + (c << s), saturating: returns false if it exceeds `hi`.
+template <typename W>
+__device__ __forceinline__ bool cell_start(const W& lo, const W& hi, unsigned c, int s, W& out);
+template <>
+__device__ __forceinline__ bool cell_start<uint16_t>(const uint16_t& lo, const uint16_t& hi, unsigned c, int s,
+                                                     uint16_t& out) {
+  const unsigned long long off = (unsigned long long)c << s;
+  if (off > (unsigned long long)(uint16_t)(hi - lo)) return false;
+  out = uint16_t(lo + off);
+  return true;
+}
+template <>
+__device__ __forceinline__ bool cell_start<uint32_t>(const uint32_t& lo, const uint32_t& hi, unsigned c, int s,
+                                                     uint32_t& out) {
+  const unsigned long long off = (unsigned long long)c << s;
+  if (off > (unsigned long long)(hi - lo)) return false;
+  out = uint32_t(lo + off);
+  return true;
+}
+template <>
+__device__ __forceinline__ bool cell_start<unsigned long long>(const unsigned long long& lo,
+                                                               const unsigned long long& hi, unsigned c, int s,
+                                                               unsigned long long& out) {
+  const unsigned long long r = hi - lo;
+  if (c == 0) {
+    out = lo;
+    return true;
+  }
+  const int cb = 32 - __clz(c);
+  if (s + cb > 64) return false;
+  const unsigned long long off = (unsigned long long)c << s;
+  if (off > r) return false;
+  out = lo + off;
+  return true;
+}
+template <>
+__device__ __forceinline__ bool cell_start<U128>(const U128& lo, const U128& hi, unsigned c, int s, U128& out) {
+  const U128 r = key_sub(hi, lo);
+  U128 off{0, 0};
+  if (c != 0) {
+    const int cb = 32 - __clz(c);
+    if (s + cb > 128) return false;
+    if (s >= 64) off = U128{0, (unsigned long long)c << (s - 64)};
+    else if (s == 0) off = U128{c, 0};
+    else off = U128{(unsigned long long)c << s, (unsigned long long)c >> (64 - s)};
+    if (key_lt(r, off)) return false;
+  }
+  const unsigned long long l = lo.lo + off.lo;
+  out = U128{l, lo.hi + off.hi + (l < lo.lo ? 1ull : 0ull)};
+  return true;
+}
+
 // Conditional swap so that a <= b afterwards (a compare-exchange).
 template <typename W>
 __device__ __forceinline__ void cas(W& a, W& b) {
@@ -132,32 +213,24 @@ __host__ __device__ __forceinline__ W flt_dec(W t, bool desc) {
   return (to & sign) ? W(to ^ sign) : W(~to);
 }
 
+// Integer transforms are one XOR with a per-call constant.
 template <typename W>
-__host__ __device__ __forceinline__ W enc(W b, int xf) {
+__host__ __device__ __forceinline__ W xf_mask(int xf) {
   constexpr int B = WordTraits<W>::kBits;
   const W sign = W(1) << (B - 1);
-  switch (xf) {
-    case XF_NOT: return W(~b);
-    case XF_SIGN: return W(b ^ sign);
-    case XF_SIGN_NOT: return W(~(b ^ sign));
-    case XF_FLT_ASC: return flt_enc<W>(b, false);
-    case XF_FLT_DESC: return flt_enc<W>(b, true);
-    default: return b;
-  }
+  return xf == XF_NOT ? W(~W(0)) : xf == XF_SIGN ? sign : xf == XF_SIGN_NOT ? W(~sign) : W(0);
+}
+
+template <typename W>
+__host__ __device__ __forceinline__ W enc(W b, int xf) {
+  if (xf >= XF_FLT_ASC) return flt_enc<W>(b, xf == XF_FLT_DESC);
+  return W(b ^ xf_mask<W>(xf));
 }
 
 template <typename W>
 __host__ __device__ __forceinline__ W dec(W t, int xf) {
-  constexpr int B = WordTraits<W>::kBits;
-  const W sign = W(1) << (B - 1);
-  switch (xf) {
-    case XF_NOT: return W(~t);
-    case XF_SIGN: return W(t ^ sign);
-    case XF_SIGN_NOT: return W((~t) ^ sign);
-    case XF_FLT_ASC: return flt_dec<W>(t, false);
-    case XF_FLT_DESC: return flt_dec<W>(t, true);
-    default: return t;
-  }
+  if (xf >= XF_FLT_ASC) return flt_dec<W>(t, xf == XF_FLT_DESC);
+  return W(t ^ xf_mask<W>(xf));
 }
 
 // 16-bit: no float type; only integer transforms.

@@ -11,9 +11,10 @@
 //                        equidistant splitters (m = 2^L - 1, L <= 8).
 //   partition.hpp:197-236 Partitioner::partition (2-way, <=pivot left)
 //                        -> k_hist + k_scatter: multiway classify with a
-//                        splitter tree in smem, warp __match_any_sync/popc
-//                        ranking, block scan, smem-staged buckets, coalesced
-//                        bucket writes; each key read+written once per level.
+//                        table-guided splitter search in smem, per-warp
+//                        shared-atomic ranking, block scan, smem-staged
+//                        buckets, coalesced bucket writes; each key is read
+//                        twice and written once per level.
 //   driver.hpp:142-151   degenerate recovery via scan_min_max -> equality
 //                        buckets: keys equal to a splitter land in a terminal
 //                        bucket, so all-equal / low-entropy inputs finish in
@@ -28,6 +29,7 @@
 
 #include "block_sort.cuh"
 #include "keys.cuh"
+#include "tile_pipe.cuh"
 
 namespace vxs {
 
@@ -60,57 +62,65 @@ struct Ctrl {
   unsigned error, pad;
 };
 
-// Compile-time configuration per key word.
+// Compile-time configuration per key word: the classify/scatter tile (keys
+// per tile), the CTA sizes of the two streaming kernels, and the base-case
+// capacity (largest class).
 template <typename W>
 struct Cfg {
-  // classify/scatter tile
-  static constexpr int kTileThreads = 256;
-  static constexpr int kTileItems = 16;
-  // base case capacity (largest class)
-  static constexpr int kCap = 8192;
-};
-template <>
-struct Cfg<uint32_t> {
-  static constexpr int kTileThreads = 512;
-  static constexpr int kTileItems = 16;
+  static constexpr int kTile = 4096;
+  static constexpr int kHistThreads = 256;
+  static constexpr int kScatThreads = 256;
   static constexpr int kCap = 8192;
 };
 template <>
 struct Cfg<uint16_t> {
-  static constexpr int kTileThreads = 512;
-  static constexpr int kTileItems = 16;
+  static constexpr int kTile = 8192;
+  static constexpr int kHistThreads = 512;
+  static constexpr int kScatThreads = 512;
   static constexpr int kCap = 8192;
 };
 template <>
 struct Cfg<U128> {
-  static constexpr int kTileThreads = 256;
-  static constexpr int kTileItems = 8;
+  static constexpr int kTile = 2048;
+  static constexpr int kHistThreads = 256;
+  static constexpr int kScatThreads = 256;
   static constexpr int kCap = 4096;
 };
+constexpr int kStages = 2;  // TMA tile pipeline depth
 
-// Base-case classes (THREADS, ITEMS); capacity THREADS*ITEMS.
+// Base-case classes (THREADS, ITEMS); capacity THREADS*ITEMS.  The smallest
+// class merges inside the warp with the __shfl_xor_sync network (WARP_NET).
 template <int C>
 struct SortClass;
 template <>
 struct SortClass<0> {
   static constexpr int T = 64, I = 4;
+  static constexpr bool kWarpNet = true;
 };
 template <>
 struct SortClass<1> {
-  static constexpr int T = 128, I = 8;
+  static constexpr int T = 64, I = 16;
+  static constexpr bool kWarpNet = false;
 };
 template <>
 struct SortClass<2> {
-  static constexpr int T = 256, I = 8;
+  static constexpr int T = 128, I = 16;
+  static constexpr bool kWarpNet = false;
 };
 template <>
 struct SortClass<3> {
   static constexpr int T = 256, I = 16;
+  static constexpr bool kWarpNet = false;
 };
 template <>
 struct SortClass<4> {
   static constexpr int T = 512, I = 16;
+  static constexpr bool kWarpNet = false;
 };
+
+// Adjacent small children are grouped into one base-case item until the
+// group holds at least this many keys (never more than Cap).
+constexpr unsigned long long kGroupTarget = 1024;
 
 __host__ __device__ inline int class_for(unsigned long long size) {
   if (size <= 256) return 0;
@@ -155,7 +165,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 template <typename W>
 __device__ __forceinline__ int ntiles_dev(unsigned long long size) {
-  constexpr int TILE = Cfg<W>::kTileThreads * Cfg<W>::kTileItems;
+  constexpr int TILE = Cfg<W>::kTile;
   return (int)((size + TILE - 1) / TILE);
 }
 
@@ -200,18 +210,53 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* total, T* scratch /*[3
   return r;
 }
 
-// Splitter tree in shared memory: tree[1..m] in BFS order of the implicit
-// balanced BST over the sorted splitters srt[0..m-1].
+// Splitters of one bucket in shared memory, with a lookup table that guides
+// classification: the key range [lo, hi] of the splitters is cut into 2^11
+// equal cells and lut[c] = #splitters < (first key of cell c).  A key's
+// child index (its lower bound among the splitters) lies in [lut[c],
+// lut[c+1]], so typical keys need one table load and 0-1 splitter
+// comparisons instead of an 8-level tree walk (binary search inside the
+// cell keeps skewed splitter sets exact and O(log)).
+constexpr int kLutBits = 11;
+constexpr int kLut = 1 << kLutBits;
+
 template <typename W>
-__device__ __forceinline__ void load_tree(const W* g_srt, int L, W* tree, W* srt) {
+struct SplSmem {
+  W srt[256];
+  W lo, hi;
+  int shift, m;
+  unsigned char lut[kLut + 8];
+};
+
+template <typename W>
+__device__ __forceinline__ int lower_bound_smem(const W* srt, int lo, int hi, const W& x) {
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (key_lt(srt[mid], x)) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+template <typename W>
+__device__ __forceinline__ void load_splitters(const W* g_srt, int L, SplSmem<W>& S) {
   const int m = (1 << L) - 1;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) srt[i] = g_srt[i];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) S.srt[i] = g_srt[i];
   __syncthreads();
-  for (int j = threadIdx.x + 1; j <= m; j += blockDim.x) {
-    const int d = 31 - __clz(j);
-    const int q = j - (1 << d);
-    const int idx = ((2 * q + 1) << (L - 1 - d)) - 1;
-    tree[j] = srt[idx];
+  if (threadIdx.x == 0) {
+    S.lo = S.srt[0];
+    S.hi = S.srt[m - 1];
+    const int bl = key_bitlen(key_sub(S.hi, S.lo));
+    S.shift = bl > kLutBits ? bl - kLutBits : 0;
+    S.m = m;
+  }
+  __syncthreads();
+  const W lo = S.lo, hi = S.hi;
+  const int sh = S.shift;
+  for (int c = threadIdx.x; c <= kLut; c += blockDim.x) {
+    W cs;
+    S.lut[c] = cell_start<W>(lo, hi, (unsigned)c, sh, cs) ? (unsigned char)lower_bound_smem(S.srt, 0, m, cs)
+                                                          : (unsigned char)m;
   }
   __syncthreads();
 }
@@ -220,14 +265,17 @@ __device__ __forceinline__ void load_tree(const W* g_srt, int L, W* tree, W* srt
 // x to the equality bucket 2i+1, else the normal bucket 2i.  Ids ascend in key
 // order: normal_0 < eq_0 < normal_1 < ... < normal_m.
 template <typename W>
-__device__ __forceinline__ int classify(const W& x, const W* tree, const W* srt, int L) {
-  int j = 1;
-#pragma unroll
-  for (int l = 0; l < kMaxL; ++l) {
-    if (l < L) j = 2 * j + (key_lt(tree[j], x) ? 1 : 0);
+__device__ __forceinline__ int classify(const W& x, const SplSmem<W>& S) {
+  int i;
+  if (!key_lt(S.lo, x)) {
+    i = 0;
+  } else if (key_lt(S.hi, x)) {
+    i = S.m;
+  } else {
+    const unsigned c = key_shr32(key_sub(x, S.lo), S.shift);
+    i = lower_bound_smem(S.srt, (int)S.lut[c], (int)S.lut[c + 1], x);
   }
-  const int i = j - (1 << L);
-  const int eq = (i < (1 << L) - 1 && key_eq(srt[i], x)) ? 1 : 0;
+  const int eq = (i < S.m && key_eq(S.srt[i], x)) ? 1 : 0;
   return 2 * i + eq;
 }
 
@@ -281,7 +329,7 @@ __global__ void k_init(Params<W> P) {
 // PAPER.md:393-398), smem bitonic sort, equidistant splitters.
 template <typename W, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   W* s = reinterpret_cast<W*>(smem_raw);
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
   const int nb = (int)(packed >> 40);
@@ -337,15 +385,49 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
   }
 }
 
-// Per-tile classification histogram (read-only pass over the level's keys).
+// Tile t of the current level: owning bucket (advanced from p), first key and
+// key count.  All threads compute the same values.
+struct TileRef {
+  int p;
+  unsigned long long lo;
+  int cnt;
+};
 template <typename W>
-__global__ void __launch_bounds__(Cfg<W>::kTileThreads) k_hist(Params<W> P) {
-  constexpr int THREADS = Cfg<W>::kTileThreads;
-  constexpr int ITEMS = Cfg<W>::kTileItems;
-  constexpr int TILE = THREADS * ITEMS;
-  __shared__ W tree[256];
-  __shared__ W srt[256];
+__device__ __forceinline__ TileRef tile_ref(const SplitDesc* list, int nb, int p, unsigned long long t) {
+  while (p + 1 < nb && list[p + 1].tile_base <= t) ++p;
+  const SplitDesc& d = list[p];
+  TileRef r;
+  r.p = p;
+  r.lo = d.start + (t - d.tile_base) * (unsigned long long)Cfg<W>::kTile;
+  const unsigned long long end = d.start + d.size;
+  r.cnt = (int)((end - r.lo) < (unsigned long long)Cfg<W>::kTile ? (end - r.lo) : Cfg<W>::kTile);
+  return r;
+}
+
+template <typename W>
+__device__ __forceinline__ const W* src_of(const Params<W>& P, unsigned flags) {
+  return (flags & F_IN_B) ? P.b : P.a;
+}
+
+template <typename W>
+__host__ __device__ constexpr int stage_bytes() {
+  return Cfg<W>::kTile * (int)sizeof(W) + 32;
+}
+
+// Per-tile classification histogram (read-only pass over the level's keys).
+// Tiles stream through a 2-stage TMA bulk-copy pipeline; counting uses plain
+// shared-memory atomics (no __match_any_sync: measured 13x slower than ATOMS
+// on B200 with ~500 distinct ids per warp); a warp whose 32 keys share one
+// child (low-entropy input) adds 32 with a single atomic.
+template <typename W>
+__global__ void __launch_bounds__(Cfg<W>::kHistThreads) k_hist(Params<W> P) {
+  constexpr int THREADS = Cfg<W>::kHistThreads;
+  constexpr int TILE = Cfg<W>::kTile;
+  constexpr int ITEMS = TILE / THREADS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ SplSmem<W> S;
   __shared__ unsigned hist[kChildStride];
+  __shared__ __align__(8) unsigned long long bars[kStages];
   __shared__ int s_p;
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
   const int nb = (int)(packed >> 40);
@@ -356,18 +438,33 @@ __global__ void __launch_bounds__(Cfg<W>::kTileThreads) k_hist(Params<W> P) {
   const unsigned long long t1 = t0 + tpc < T ? t0 + tpc : T;
   if (t0 >= t1) return;
   const SplitDesc* list = P.split[P.cur];
-  if (threadIdx.x == 0) s_p = find_bucket(list, nb, t0);
+  int p_issue = 0;
+  if (threadIdx.x == 0) {
+    s_p = find_bucket(list, nb, t0);
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    p_issue = s_p;
+    const TileRef r = tile_ref<W>(list, nb, p_issue, t0);
+    tile_issue(src_of(P, list[r.p].flags) + r.lo, (unsigned long long)r.cnt * sizeof(W), smem_raw, &bars[0]);
+  }
   for (int i = threadIdx.x; i < kChildStride; i += THREADS) hist[i] = 0;
   __syncthreads();
   int p = s_p;
   SplitDesc d = list[p];
   int L = (int)d.L;
-  load_tree(P.splitters + (unsigned long long)p * 256, L, tree, srt);
+  load_splitters(P.splitters + (unsigned long long)p * 256, L, S);
   const int lane = threadIdx.x & 31;
+  unsigned phase = 0;
   for (unsigned long long t = t0; t < t1; ++t) {
+    const int st = (int)((t - t0) & (kStages - 1));
+    if (threadIdx.x == 0 && t + 1 < t1) {
+      const TileRef r = tile_ref<W>(list, nb, p_issue, t + 1);
+      p_issue = r.p;
+      tile_issue(src_of(P, list[r.p].flags) + r.lo, (unsigned long long)r.cnt * sizeof(W),
+                 smem_raw + (st ^ 1) * stage_bytes<W>(), &bars[st ^ 1]);
+    }
     if (p + 1 < nb && list[p + 1].tile_base <= t) {
       // flush and move to the next bucket
-      __syncthreads();
       const int nc = 2 * ((1 << L) - 1) + 1;
       for (int c = threadIdx.x; c < nc; c += THREADS) {
         if (hist[c]) atomicAdd(P.counts + (unsigned long long)p * kChildStride + c, (unsigned long long)hist[c]);
@@ -377,32 +474,38 @@ __global__ void __launch_bounds__(Cfg<W>::kTileThreads) k_hist(Params<W> P) {
       d = list[p];
       L = (int)d.L;
       __syncthreads();
-      load_tree(P.splitters + (unsigned long long)p * 256, L, tree, srt);
+      load_splitters(P.splitters + (unsigned long long)p * 256, L, S);
     }
-    const W* src = (d.flags & F_IN_B) ? P.b : P.a;
+    const W* src = src_of(P, d.flags);
     const int xf = (d.flags & F_RAW) ? P.xf : XF_NONE;
     const unsigned long long lo = d.start + (t - d.tile_base) * TILE;
     const unsigned long long end = d.start + d.size;
     const int cnt = (int)((end - lo) < (unsigned long long)TILE ? (end - lo) : TILE);
-    W k[ITEMS];
+    const TileSpan span = tile_span(src + lo, (unsigned long long)cnt * sizeof(W));
+    const unsigned char* stage = smem_raw + st * stage_bytes<W>();
+    mbar_wait(&bars[st], (phase >> st) & 1);
+    phase ^= 1u << st;
+    int bk[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const int idx = i * THREADS + threadIdx.x;
-      k[i] = idx < cnt ? enc<W>(ldcs(src + lo + idx), xf) : key_max<W>();
+      const W x = idx < cnt ? enc<W>(tile_key(src + lo, idx, span, stage), xf) : key_max<W>();
+      bk[i] = classify(x, S);
     }
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const int idx = i * THREADS + threadIdx.x;
       const bool valid = idx < cnt;
-      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-      if (valid) {
-        const int b = classify(k[i], tree, srt, L);
-        const unsigned peers = __match_any_sync(vmask, b);
-        if (lane == __ffs(peers) - 1) atomicAdd(&hist[b], (unsigned)__popc(peers));
+      const int b0 = __shfl_sync(0xffffffffu, bk[i], 0);
+      const bool uni = __all_sync(0xffffffffu, valid && bk[i] == b0);
+      if (uni) {
+        if (lane == 0) atomicAdd(&hist[b0], 32u);
+      } else if (valid) {
+        atomicAdd(&hist[bk[i]], 1u);
       }
     }
+    __syncthreads();  // stage st fully consumed before it is refilled
   }
-  __syncthreads();
   const int nc = 2 * ((1 << L) - 1) + 1;
   for (int c = threadIdx.x; c < nc; c += THREADS) {
     if (hist[c]) atomicAdd(P.counts + (unsigned long long)p * kChildStride + c, (unsigned long long)hist[c]);
@@ -507,7 +610,7 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
           }
           continue;
         }
-        if (gz + s > CAP) emit();
+        if (gz + s > CAP || gz >= kGroupTarget) emit();
         if (gz == 0) gs = d.start + s_off[ch];
         gz += s;
         gsort = gsort || (!eq && s > 1);
@@ -558,24 +661,26 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
   }
 }
 
-// Scatter: classify again, rank within the tile per child with warp-aggregated
-// smem atomics (__match_any_sync + popc), block scan, stage the tile in smem
-// grouped by child, reserve each child's global range with one atomic per
-// (tile, child), then write each child run with consecutive threads.
+// Scatter: classify again, rank each key within its (warp, child) with a
+// returning shared atomic on a per-warp histogram, scan across warps and
+// children, stage the tile in smem grouped by child (reusing the tile's TMA
+// stage), reserve each child's global range with one atomic per (tile,
+// child), then write each child run with consecutive threads (coalesced).
 template <typename W>
-__global__ void __launch_bounds__(Cfg<W>::kTileThreads) k_scatter(Params<W> P) {
-  constexpr int THREADS = Cfg<W>::kTileThreads;
-  constexpr int ITEMS = Cfg<W>::kTileItems;
-  constexpr int TILE = THREADS * ITEMS;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  W* stage = reinterpret_cast<W*>(smem_raw);
-  unsigned short* stage_b = reinterpret_cast<unsigned short*>(stage + TILE);
-  __shared__ W tree[256];
-  __shared__ W srt[256];
-  __shared__ unsigned hist[kChildStride];
+__global__ void __launch_bounds__(Cfg<W>::kScatThreads) k_scatter(Params<W> P) {
+  constexpr int THREADS = Cfg<W>::kScatThreads;
+  constexpr int TILE = Cfg<W>::kTile;
+  constexpr int ITEMS = TILE / THREADS;
+  constexpr int NW = THREADS / 32;
+  constexpr int PER = kChildStride / THREADS > 0 ? kChildStride / THREADS : 1;  // children per thread
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned short* stage_b = reinterpret_cast<unsigned short*>(smem_raw + kStages * stage_bytes<W>());
+  unsigned* whist = reinterpret_cast<unsigned*>(stage_b + TILE);  // [NW][kChildStride]
+  __shared__ SplSmem<W> S;
   __shared__ unsigned toff[kChildStride];
   __shared__ unsigned long long gbase[kChildStride];
   __shared__ unsigned scan_scratch[32];
+  __shared__ __align__(8) unsigned long long bars[kStages];
   __shared__ int s_p;
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
   const int nb = (int)(packed >> 40);
@@ -586,88 +691,116 @@ __global__ void __launch_bounds__(Cfg<W>::kTileThreads) k_scatter(Params<W> P) {
   const unsigned long long t1 = t0 + tpc < T ? t0 + tpc : T;
   if (t0 >= t1) return;
   const SplitDesc* list = P.split[P.cur];
-  if (threadIdx.x == 0) s_p = find_bucket(list, nb, t0);
+  int p_issue = 0;
+  if (threadIdx.x == 0) {
+    s_p = find_bucket(list, nb, t0);
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    p_issue = s_p;
+    const TileRef r = tile_ref<W>(list, nb, p_issue, t0);
+    tile_issue(src_of(P, list[r.p].flags) + r.lo, (unsigned long long)r.cnt * sizeof(W), smem_raw, &bars[0]);
+  }
   __syncthreads();
   int p = s_p;
   SplitDesc d = list[p];
   int L = (int)d.L;
-  load_tree(P.splitters + (unsigned long long)p * 256, L, tree, srt);
+  load_splitters(P.splitters + (unsigned long long)p * 256, L, S);
   const int lane = threadIdx.x & 31;
-  W* dst_buf = P.part_mode ? P.out : ((d.flags & F_IN_B) ? P.a : P.b);
+  const int warp = threadIdx.x >> 5;
+  unsigned* myhist = whist + warp * kChildStride;
   const int out_xf = P.part_mode ? P.xf : XF_NONE;
+  unsigned phase = 0;
   for (unsigned long long t = t0; t < t1; ++t) {
+    const int st = (int)((t - t0) & (kStages - 1));
+    if (threadIdx.x == 0 && t + 1 < t1) {
+      const TileRef r = tile_ref<W>(list, nb, p_issue, t + 1);
+      p_issue = r.p;
+      tile_issue(src_of(P, list[r.p].flags) + r.lo, (unsigned long long)r.cnt * sizeof(W),
+                 smem_raw + (st ^ 1) * stage_bytes<W>(), &bars[st ^ 1]);
+    }
     if (p + 1 < nb && list[p + 1].tile_base <= t) {
       while (p + 1 < nb && list[p + 1].tile_base <= t) ++p;
       d = list[p];
       L = (int)d.L;
-      dst_buf = P.part_mode ? P.out : ((d.flags & F_IN_B) ? P.a : P.b);
-      load_tree(P.splitters + (unsigned long long)p * 256, L, tree, srt);
+      load_splitters(P.splitters + (unsigned long long)p * 256, L, S);
     }
+    W* dst_buf = P.part_mode ? P.out : ((d.flags & F_IN_B) ? P.a : P.b);
     const int nc = 2 * ((1 << L) - 1) + 1;
-    for (int i = threadIdx.x; i < kChildStride; i += THREADS) hist[i] = 0;
-    const W* src = (d.flags & F_IN_B) ? P.b : P.a;
+    for (int i = threadIdx.x; i < NW * kChildStride; i += THREADS) whist[i] = 0;
+    const W* src = src_of(P, d.flags);
     const int xf = (d.flags & F_RAW) ? P.xf : XF_NONE;
     const unsigned long long lo = d.start + (t - d.tile_base) * TILE;
     const unsigned long long end = d.start + d.size;
     const int cnt = (int)((end - lo) < (unsigned long long)TILE ? (end - lo) : TILE);
+    const TileSpan span = tile_span(src + lo, (unsigned long long)cnt * sizeof(W));
+    unsigned char* stage = smem_raw + st * stage_bytes<W>();
+    mbar_wait(&bars[st], (phase >> st) & 1);
+    phase ^= 1u << st;
     W k[ITEMS];
     int bk[ITEMS];
     unsigned rk[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const int idx = i * THREADS + threadIdx.x;
-      k[i] = idx < cnt ? enc<W>(ldcs(src + lo + idx), xf) : key_max<W>();
+      k[i] = idx < cnt ? enc<W>(tile_key(src + lo, idx, span, stage), xf) : key_max<W>();
+      bk[i] = classify(k[i], S);
     }
-    __syncthreads();  // hist zeroed
+    __syncthreads();  // whist zeroed; stage st consumed (reused for staging below)
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const int idx = i * THREADS + threadIdx.x;
       const bool valid = idx < cnt;
-      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-      bk[i] = -1;
-      rk[i] = 0;
-      if (valid) {
-        const int b = classify(k[i], tree, srt, L);
-        const unsigned peers = __match_any_sync(vmask, b);
-        const int leader = __ffs(peers) - 1;
+      if (!valid) bk[i] = -1;
+      const int b0 = __shfl_sync(0xffffffffu, bk[i], 0);
+      const bool uni = __all_sync(0xffffffffu, bk[i] == b0) && b0 >= 0;
+      if (uni) {
         unsigned base = 0;
-        if (lane == leader) base = atomicAdd(&hist[b], (unsigned)__popc(peers));
-        base = __shfl_sync(peers, base, leader);
-        bk[i] = b;
-        rk[i] = base + __popc(peers & lanemask_lt());
+        if (lane == 0) base = atomicAdd(&myhist[b0], 32u);
+        rk[i] = __shfl_sync(0xffffffffu, base, 0) + lane;
+      } else if (valid) {
+        rk[i] = atomicAdd(&myhist[bk[i]], 1u);
       }
     }
     __syncthreads();
-    // exclusive scan of the tile histogram (THREADS >= 256 -> 2 per thread max)
+    // per child: exclusive prefix across warps (in place), then across children
     {
-      constexpr int PER = kChildStride / THREADS > 0 ? kChildStride / THREADS : 1;
-      unsigned v[PER];
+      unsigned tot[PER];
       unsigned sum = 0;
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
         const int c = threadIdx.x * PER + j;
-        v[j] = c < kChildStride ? hist[c] : 0;
-        sum += v[j];
+        unsigned run = 0;
+        if (c < kChildStride) {
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            const unsigned v = whist[w * kChildStride + c];
+            whist[w * kChildStride + c] = run;
+            run += v;
+          }
+        }
+        tot[j] = run;
+        sum += run;
       }
-      unsigned tot;
-      unsigned ex = block_exclusive_scan<THREADS>(sum, &tot, scan_scratch);
+      unsigned total;
+      unsigned ex = block_exclusive_scan<THREADS>(sum, &total, scan_scratch);
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
         const int c = threadIdx.x * PER + j;
         if (c < kChildStride) {
           toff[c] = ex;
-          if (v[j] && c < nc)
-            gbase[c] = atomicAdd(P.cursors + (unsigned long long)p * kChildStride + c, (unsigned long long)v[j]);
+          if (tot[j] && c < nc)
+            gbase[c] = atomicAdd(P.cursors + (unsigned long long)p * kChildStride + c, (unsigned long long)tot[j]);
         }
-        ex += v[j];
+        ex += tot[j];
       }
     }
     __syncthreads();
+    W* staged = reinterpret_cast<W*>(stage);
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       if (bk[i] >= 0) {
-        const unsigned pos = toff[bk[i]] + rk[i];
-        stage[pos] = k[i];
+        const unsigned pos = toff[bk[i]] + myhist[bk[i]] + rk[i];
+        staged[pos] = k[i];
         stage_b[pos] = (unsigned short)bk[i];
       }
     }
@@ -675,7 +808,7 @@ __global__ void __launch_bounds__(Cfg<W>::kTileThreads) k_scatter(Params<W> P) {
     for (int j = threadIdx.x; j < cnt; j += THREADS) {
       const int c = stage_b[j];
       const unsigned long long dst = gbase[c] + (unsigned long long)(j - (int)toff[c]);
-      dst_buf[dst] = dec<W>(stage[j], out_xf);
+      dst_buf[dst] = dec<W>(staged[j], out_xf);
     }
     __syncthreads();
   }
@@ -688,7 +821,7 @@ __global__ void __launch_bounds__(SortClass<CLS>::T) k_final(Params<W> P) {
   constexpr int THREADS = SortClass<CLS>::T;
   constexpr int ITEMS = SortClass<CLS>::I;
   constexpr int TOTAL = THREADS * ITEMS;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   W* sm = reinterpret_cast<W*>(smem_raw);
   const unsigned long long nitems = P.ctrl->item_count[CLS];
   const Item* items = P.items[CLS];
@@ -703,12 +836,12 @@ __global__ void __launch_bounds__(SortClass<CLS>::T) k_final(Params<W> P) {
       const int idx = i * THREADS + threadIdx.x;
       k[i] = idx < size ? enc<W>(ldcs(src + item.start + idx), xf) : key_max<W>();
     }
-    block_sort<W, THREADS, ITEMS>(k, sm);
+    block_sort<W, THREADS, ITEMS, SortClass<CLS>::kWarpNet>(k, sm);
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) sm[threadIdx.x * ITEMS + i] = k[i];
+    for (int i = 0; i < ITEMS; ++i) sm[pad_idx<W>(threadIdx.x * ITEMS + i)] = k[i];
     __syncthreads();
     W* dst = P.a + item.start;
-    for (int idx = threadIdx.x; idx < size; idx += THREADS) dst[idx] = dec<W>(sm[idx], P.xf);
+    for (int idx = threadIdx.x; idx < size; idx += THREADS) dst[idx] = dec<W>(sm[pad_idx<W>(idx)], P.xf);
     __syncthreads();
   }
   (void)TOTAL;

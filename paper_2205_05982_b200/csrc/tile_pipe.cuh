@@ -1,0 +1,96 @@
+// tile_pipe.cuh -- TMA bulk-copy (cp.async.bulk) tile pipeline for the
+// streaming kernels.
+//
+// One elected thread issues `cp.async.bulk.shared::cluster.global` for the
+// NEXT tile of keys into a shared-memory stage while the CTA classifies the
+// current one; completion is tracked by a transaction-count mbarrier per
+// stage.  The copy covers the 16-byte-aligned middle of the tile's byte
+// range; the few keys in the unaligned head/tail (< 16 bytes each side) are
+// read straight from global memory by the consumer.
+#pragma once
+#include <cstdint>
+
+#include "keys.cuh"
+
+namespace vxs {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Byte geometry of one tile [addr, addr + bytes) in global memory.
+struct TileSpan {
+  unsigned long long base;  // addr rounded down to 16
+  unsigned long long a0;    // first 16-aligned byte inside the tile
+  unsigned long long a1;    // end of the last full 16-byte chunk inside the tile
+};
+
+__device__ __forceinline__ TileSpan tile_span(const void* p, unsigned long long bytes) {
+  const unsigned long long addr = reinterpret_cast<unsigned long long>(p);
+  TileSpan s;
+  s.base = addr & ~15ull;
+  s.a0 = (addr + 15) & ~15ull;
+  s.a1 = (addr + bytes) & ~15ull;
+  if (s.a1 < s.a0) s.a1 = s.a0;
+  return s;
+}
+
+// Thread 0 only: start copying the aligned middle of the tile into `stage`
+// (stage byte 0 == global byte s.base).  Always arrives on the barrier, so
+// a tile with no aligned middle completes immediately.
+__device__ __forceinline__ void tile_issue(const void* p, unsigned long long bytes, unsigned char* stage,
+                                           unsigned long long* bar) {
+  const TileSpan s = tile_span(p, bytes);
+  const unsigned n = (unsigned)(s.a1 - s.a0);
+  fence_proxy_async_smem();
+  mbar_arrive_expect_tx(bar, n);
+  if (n) bulk_g2s(stage + (s.a0 - s.base), reinterpret_cast<const void*>(s.a0), n, bar);
+}
+
+// Consumer read of key j of a tile whose first key is at global `g`.
+template <typename W>
+__device__ __forceinline__ W tile_key(const W* g, int j, const TileSpan& s, const unsigned char* stage) {
+  const unsigned long long a = reinterpret_cast<unsigned long long>(g + j);
+  if (a >= s.a0 && a + sizeof(W) <= s.a1) return *reinterpret_cast<const W*>(stage + (a - s.base));
+  return ldcs(g + j);
+}
+
+}  // namespace vxs

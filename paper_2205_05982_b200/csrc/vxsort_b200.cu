@@ -177,8 +177,13 @@ constexpr size_t sample_smem() {
   return kMaxSamples * sizeof(W);
 }
 template <typename W>
+constexpr size_t hist_smem() {
+  return (size_t)kStages * stage_bytes<W>();
+}
+template <typename W>
 constexpr size_t scatter_smem() {
-  return (size_t)Cfg<W>::kTileThreads * Cfg<W>::kTileItems * (sizeof(W) + sizeof(unsigned short));
+  return (size_t)kStages * stage_bytes<W>() + (size_t)Cfg<W>::kTile * sizeof(unsigned short) +
+         (size_t)(Cfg<W>::kScatThreads / 32) * kChildStride * sizeof(unsigned);
 }
 
 // Levels a uniform input of n keys needs (>=128-way shrink per level).
@@ -204,8 +209,8 @@ vxs_status launch_level(Params<W>& P, cudaStream_t st, int& launches) {
   {
     ProfScope ps(K_HIST, st);
     auto fn = k_hist<W>;
-    const int g = grid_for((const void*)fn, Cfg<W>::kTileThreads, 0);
-    fn<<<g, Cfg<W>::kTileThreads, 0, st>>>(P);
+    const int g = grid_for((const void*)fn, Cfg<W>::kHistThreads, hist_smem<W>());
+    fn<<<g, Cfg<W>::kHistThreads, hist_smem<W>(), st>>>(P);
   }
   {
     ProfScope ps(K_PLAN, st);
@@ -216,8 +221,8 @@ vxs_status launch_level(Params<W>& P, cudaStream_t st, int& launches) {
   {
     ProfScope ps(K_SCATTER, st);
     auto fn = k_scatter<W>;
-    const int g = grid_for((const void*)fn, Cfg<W>::kTileThreads, scatter_smem<W>());
-    fn<<<g, Cfg<W>::kTileThreads, scatter_smem<W>(), st>>>(P);
+    const int g = grid_for((const void*)fn, Cfg<W>::kScatThreads, scatter_smem<W>());
+    fn<<<g, Cfg<W>::kScatThreads, scatter_smem<W>(), st>>>(P);
   }
   launches += 4;
   VXS_CK(cudaGetLastError(), "level launch");
@@ -227,7 +232,7 @@ vxs_status launch_level(Params<W>& P, cudaStream_t st, int& launches) {
 template <typename W, int CLS>
 void launch_final(Params<W>& P, unsigned long long count, cudaStream_t st) {
   constexpr int T = SortClass<CLS>::T;
-  constexpr size_t smem = (size_t)T * SortClass<CLS>::I * sizeof(W);
+  constexpr size_t smem = (size_t)padded_size<W>(T * SortClass<CLS>::I) * sizeof(W);
   ProfScope ps(K_FINAL0 + CLS, st);
   auto fn = k_final<W, CLS>;
   int g = grid_for((const void*)fn, T, smem);
@@ -550,14 +555,14 @@ vxs_status vxs_partition(const void* d_keys, size_t n, vxs_key_type type, vxs_or
     k_part_setup<W><<<1, 256, 0, st>>>(P, static_cast<const W*>(d_splitters), nspl, L);
     {
       auto fn = k_hist<W>;
-      const int g = grid_for((const void*)fn, Cfg<W>::kTileThreads, 0);
-      fn<<<g, Cfg<W>::kTileThreads, 0, st>>>(P);
+      const int g = grid_for((const void*)fn, Cfg<W>::kHistThreads, hist_smem<W>());
+      fn<<<g, Cfg<W>::kHistThreads, hist_smem<W>(), st>>>(P);
     }
     k_plan<W><<<1, kChildStride, 0, st>>>(P);
     {
       auto fn = k_scatter<W>;
-      const int g = grid_for((const void*)fn, Cfg<W>::kTileThreads, scatter_smem<W>());
-      fn<<<g, Cfg<W>::kTileThreads, scatter_smem<W>(), st>>>(P);
+      const int g = grid_for((const void*)fn, Cfg<W>::kScatThreads, scatter_smem<W>());
+      fn<<<g, Cfg<W>::kScatThreads, scatter_smem<W>(), st>>>(P);
     }
     k_part_counts<W><<<1, 256, 0, st>>>(P, nseg, reinterpret_cast<unsigned long long*>(d_seg_counts));
     VXS_CK(cudaGetLastError(), "partition");
