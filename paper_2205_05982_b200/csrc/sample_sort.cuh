@@ -222,10 +222,11 @@ constexpr int kLut = 1 << kLutBits;
 
 template <typename W>
 struct SplSmem {
-  W srt[256];
-  W lo, hi;
+  W srt[257];  // m splitters + sentinel
+  W lo;
+  unsigned cmax;
   int shift, m;
-  unsigned char lut[kLut + 8];
+  unsigned short lut[kLut];  // (first, end) splitter index of cell c, packed lo | hi << 8
 };
 
 template <typename W>
@@ -240,41 +241,53 @@ __device__ __forceinline__ int lower_bound_smem(const W* srt, int lo, int hi, co
 
 template <typename W>
 __device__ __forceinline__ void load_splitters(const W* g_srt, int L, SplSmem<W>& S) {
+  __shared__ unsigned char first[kLut + 1];
   const int m = (1 << L) - 1;
   for (int i = threadIdx.x; i < m; i += blockDim.x) S.srt[i] = g_srt[i];
+  if (threadIdx.x == 0) S.srt[m] = key_max<W>();
   __syncthreads();
   if (threadIdx.x == 0) {
     S.lo = S.srt[0];
-    S.hi = S.srt[m - 1];
-    const int bl = key_bitlen(key_sub(S.hi, S.lo));
+    const W range = key_sub(S.srt[m - 1], S.lo);
+    const int bl = key_bitlen(range);
     S.shift = bl > kLutBits ? bl - kLutBits : 0;
+    S.cmax = key_shr32(range, S.shift);
     S.m = m;
   }
   __syncthreads();
-  const W lo = S.lo, hi = S.hi;
+  const W lo = S.lo, hi = S.srt[m - 1];
   const int sh = S.shift;
   for (int c = threadIdx.x; c <= kLut; c += blockDim.x) {
     W cs;
-    S.lut[c] = cell_start<W>(lo, hi, (unsigned)c, sh, cs) ? (unsigned char)lower_bound_smem(S.srt, 0, m, cs)
+    first[c] = cell_start<W>(lo, hi, (unsigned)c, sh, cs) ? (unsigned char)lower_bound_smem(S.srt, 0, m, cs)
                                                           : (unsigned char)m;
   }
+  __syncthreads();
+  for (int c = threadIdx.x; c < kLut; c += blockDim.x)
+    S.lut[c] = (unsigned short)(first[c] | ((unsigned)first[c + 1] << 8));
   __syncthreads();
 }
 
 // Child id of key x: i = #splitters < x (lower bound); an equal splitter sends
 // x to the equality bucket 2i+1, else the normal bucket 2i.  Ids ascend in key
-// order: normal_0 < eq_0 < normal_1 < ... < normal_m.
+// order: normal_0 < eq_0 < normal_1 < ... < normal_m.  Keys below the first
+// splitter use cell 0, keys above the last use the last cell; the answer
+// always lies in [first(c), end(c)].
 template <typename W>
 __device__ __forceinline__ int classify(const W& x, const SplSmem<W>& S) {
-  int i;
-  if (!key_lt(S.lo, x)) {
-    i = 0;
-  } else if (key_lt(S.hi, x)) {
-    i = S.m;
-  } else {
-    const unsigned c = key_shr32(key_sub(x, S.lo), S.shift);
-    i = lower_bound_smem(S.srt, (int)S.lut[c], (int)S.lut[c + 1], x);
+  unsigned c = key_shr32(key_sub(x, S.lo), S.shift);
+  c = c < S.cmax ? c : S.cmax;
+  c = key_lt(x, S.lo) ? 0u : c;
+  const unsigned pr = S.lut[c];
+  int i = (int)(pr & 0xFFu);
+  int e = (int)(pr >> 8);
+  while (e - i > 2) {  // rare: more than two splitters in one cell
+    const int mid = (i + e) >> 1;
+    if (key_lt(S.srt[mid], x)) i = mid + 1;
+    else e = mid;
   }
+  i += (i < e && key_lt(S.srt[i], x)) ? 1 : 0;
+  i += (i < e && key_lt(S.srt[i], x)) ? 1 : 0;
   const int eq = (i < S.m && key_eq(S.srt[i], x)) ? 1 : 0;
   return 2 * i + eq;
 }
@@ -453,7 +466,6 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads) k_hist(Params<W> P) {
   SplitDesc d = list[p];
   int L = (int)d.L;
   load_splitters(P.splitters + (unsigned long long)p * 256, L, S);
-  const int lane = threadIdx.x & 31;
   unsigned phase = 0;
   for (unsigned long long t = t0; t < t1; ++t) {
     const int st = (int)((t - t0) & (kStages - 1));
@@ -482,27 +494,15 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads) k_hist(Params<W> P) {
     const unsigned long long end = d.start + d.size;
     const int cnt = (int)((end - lo) < (unsigned long long)TILE ? (end - lo) : TILE);
     const TileSpan span = tile_span(src + lo, (unsigned long long)cnt * sizeof(W));
-    const unsigned char* stage = smem_raw + st * stage_bytes<W>();
+    unsigned char* stage = smem_raw + st * stage_bytes<W>();
     mbar_wait(&bars[st], (phase >> st) & 1);
     phase ^= 1u << st;
-    int bk[ITEMS];
+    const unsigned char* kp = tile_fixup<W, THREADS>(src + lo, cnt, span, stage);
+    __syncthreads();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const int idx = i * THREADS + threadIdx.x;
-      const W x = idx < cnt ? enc<W>(tile_key(src + lo, idx, span, stage), xf) : key_max<W>();
-      bk[i] = classify(x, S);
-    }
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const int idx = i * THREADS + threadIdx.x;
-      const bool valid = idx < cnt;
-      const int b0 = __shfl_sync(0xffffffffu, bk[i], 0);
-      const bool uni = __all_sync(0xffffffffu, valid && bk[i] == b0);
-      if (uni) {
-        if (lane == 0) atomicAdd(&hist[b0], 32u);
-      } else if (valid) {
-        atomicAdd(&hist[bk[i]], 1u);
-      }
+      if (idx < cnt) atomicAdd(&hist[classify(enc<W>(lds_key<W>(kp, idx), xf), S)], 1u);
     }
     __syncthreads();  // stage st fully consumed before it is refilled
   }
@@ -736,13 +736,15 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads) k_scatter(Params<W> P) {
     unsigned char* stage = smem_raw + st * stage_bytes<W>();
     mbar_wait(&bars[st], (phase >> st) & 1);
     phase ^= 1u << st;
+    const unsigned char* kp = tile_fixup<W, THREADS>(src + lo, cnt, span, stage);
+    __syncthreads();
     W k[ITEMS];
     int bk[ITEMS];
     unsigned rk[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const int idx = i * THREADS + threadIdx.x;
-      k[i] = idx < cnt ? enc<W>(tile_key(src + lo, idx, span, stage), xf) : key_max<W>();
+      k[i] = idx < cnt ? enc<W>(lds_key<W>(kp, idx), xf) : key_max<W>();
       bk[i] = classify(k[i], S);
     }
     __syncthreads();  // whist zeroed; stage st consumed (reused for staging below)
@@ -836,7 +838,10 @@ __global__ void __launch_bounds__(SortClass<CLS>::T) k_final(Params<W> P) {
       const int idx = i * THREADS + threadIdx.x;
       k[i] = idx < size ? enc<W>(ldcs(src + item.start + idx), xf) : key_max<W>();
     }
-    block_sort<W, THREADS, ITEMS, SortClass<CLS>::kWarpNet>(k, sm);
+    // 32-bit and narrower keys merge inside the warp with __shfl_xor_sync
+    // networks (measured faster); 64/128-bit keys use shared-memory merge path.
+    constexpr bool kWN = SortClass<CLS>::kWarpNet || sizeof(W) <= 4;
+    block_sort<W, THREADS, ITEMS, kWN>(k, sm);
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) sm[pad_idx<W>(threadIdx.x * ITEMS + i)] = k[i];
     __syncthreads();

@@ -94,3 +94,45 @@ __device__ __forceinline__ W tile_key(const W* g, int j, const TileSpan& s, cons
 }
 
 }  // namespace vxs
+
+namespace vxs {
+
+// Shared-memory key access at byte pointer p (K128 may be only 8-aligned).
+template <typename W>
+__device__ __forceinline__ W lds_key(const unsigned char* p, int j) {
+  return reinterpret_cast<const W*>(p)[j];
+}
+template <>
+__device__ __forceinline__ U128 lds_key<U128>(const unsigned char* p, int j) {
+  const unsigned long long* q = reinterpret_cast<const unsigned long long*>(p) + 2 * j;
+  return U128{q[0], q[1]};
+}
+template <typename W>
+__device__ __forceinline__ void sts_key(unsigned char* p, int j, const W& v) {
+  reinterpret_cast<W*>(p)[j] = v;
+}
+template <>
+__device__ __forceinline__ void sts_key<U128>(unsigned char* p, int j, const U128& v) {
+  unsigned long long* q = reinterpret_cast<unsigned long long*>(p) + 2 * j;
+  q[0] = v.lo;
+  q[1] = v.hi;
+}
+
+// After the stage's barrier completed: load the (< 16 bytes each side) head
+// and tail keys the bulk copy did not cover, so the whole tile is in smem.
+// Returns the smem address of key 0.  Caller must __syncthreads() before
+// reading keys written by other threads.
+template <typename W, int THREADS>
+__device__ __forceinline__ unsigned char* tile_fixup(const W* g, int cnt, const TileSpan& s, unsigned char* stage) {
+  const unsigned long long addr = reinterpret_cast<unsigned long long>(g);
+  unsigned char* k0 = stage + (addr - s.base);
+  long long h = (long long)((s.a0 - addr + sizeof(W) - 1) / sizeof(W));
+  if (h > cnt) h = cnt;
+  long long tl = s.a1 > addr ? (long long)((s.a1 - addr) / sizeof(W)) : 0;
+  if (tl < h) tl = h;
+  for (int j = threadIdx.x; j < h; j += THREADS) sts_key<W>(k0, j, ldcs(g + j));
+  for (long long j = tl + threadIdx.x; j < cnt; j += THREADS) sts_key<W>(k0, (int)j, ldcs(g + j));
+  return k0;
+}
+
+}  // namespace vxs
