@@ -400,7 +400,8 @@ def run_single(args):
                          "design_hbm_frac": round(algorithmic_bytes(ste, ne, kbe)["total"] / (mse * 1e-3) / 1e9
                                                   / peak, 4),
                          "scatter_frac": (round(sc["bytes_per_sort"] / (sc["ms"] / 3 * 1e-3) / 1e9 / peak, 4)
-                                          if sc else None)}
+                                          if sc else None),
+                         "kernels_ms": {k: round(v[1] / 3, 4) for k, v in pre.items()}}
             del se, be, wse
             torch.cuda.empty_cache()
         line["extra"] = extra

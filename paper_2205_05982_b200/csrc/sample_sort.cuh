@@ -272,24 +272,39 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, int L, SplSmem<W>
 // x to the equality bucket 2i+1, else the normal bucket 2i.  Ids ascend in key
 // order: normal_0 < eq_0 < normal_1 < ... < normal_m.  Keys below the first
 // splitter use cell 0, keys above the last use the last cell; the answer
-// always lies in [first(c), end(c)].
+// always lies in [first(c), end(c)] and srt[end(c)] >= x (sentinel srt[m] =
+// max), so two unguarded steps finish any cell holding <= 2 splitters.
+// classify_fast returns -1 for the rare wider cells (skewed splitter sets);
+// classify_slow resolves those with a binary search.
 template <typename W>
-__device__ __forceinline__ int classify(const W& x, const SplSmem<W>& S) {
+__device__ __forceinline__ int classify_fast(const W& x, const SplSmem<W>& S) {
   unsigned c = key_shr32(key_sub(x, S.lo), S.shift);
   c = c < S.cmax ? c : S.cmax;
   c = key_lt(x, S.lo) ? 0u : c;
   const unsigned pr = S.lut[c];
   int i = (int)(pr & 0xFFu);
-  int e = (int)(pr >> 8);
-  while (e - i > 2) {  // rare: more than two splitters in one cell
-    const int mid = (i + e) >> 1;
-    if (key_lt(S.srt[mid], x)) i = mid + 1;
-    else e = mid;
-  }
-  i += (i < e && key_lt(S.srt[i], x)) ? 1 : 0;
-  i += (i < e && key_lt(S.srt[i], x)) ? 1 : 0;
+  const int e = (int)(pr >> 8);
+  i += key_lt(S.srt[i], x) ? 1 : 0;
+  i += key_lt(S.srt[i], x) ? 1 : 0;
+  const int eq = (key_eq(S.srt[i], x) && i < S.m) ? 1 : 0;
+  return e - (int)(pr & 0xFFu) > 2 ? -1 : 2 * i + eq;
+}
+
+template <typename W>
+__device__ __noinline__ int classify_slow(const W& x, const SplSmem<W>& S) {
+  unsigned c = key_shr32(key_sub(x, S.lo), S.shift);
+  c = c < S.cmax ? c : S.cmax;
+  c = key_lt(x, S.lo) ? 0u : c;
+  const unsigned pr = S.lut[c];
+  const int i = lower_bound_smem(S.srt, (int)(pr & 0xFFu), (int)(pr >> 8), x);
   const int eq = (i < S.m && key_eq(S.srt[i], x)) ? 1 : 0;
   return 2 * i + eq;
+}
+
+template <typename W>
+__device__ __forceinline__ int classify(const W& x, const SplSmem<W>& S) {
+  const int b = classify_fast(x, S);
+  return b >= 0 ? b : classify_slow(x, S);
 }
 
 // Find the split bucket owning global tile t (binary search on tile_base).
@@ -499,10 +514,29 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads) k_hist(Params<W> P) {
     phase ^= 1u << st;
     const unsigned char* kp = tile_fixup<W, THREADS>(src + lo, cnt, span, stage);
     __syncthreads();
+    unsigned wide = 0;  // items whose cell holds > 2 splitters (rare)
+    if (cnt == TILE) {
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const int idx = i * THREADS + threadIdx.x;
-      if (idx < cnt) atomicAdd(&hist[classify(enc<W>(lds_key<W>(kp, idx), xf), S)], 1u);
+      for (int i = 0; i < ITEMS; ++i) {
+        const int b = classify_fast(enc<W>(lds_key<W>(kp, i * THREADS + threadIdx.x), xf), S);
+        if (b >= 0) atomicAdd(&hist[b], 1u);
+        else wide |= 1u << i;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int idx = i * THREADS + threadIdx.x;
+        if (idx < cnt) {
+          const int b = classify_fast(enc<W>(lds_key<W>(kp, idx), xf), S);
+          if (b >= 0) atomicAdd(&hist[b], 1u);
+          else wide |= 1u << i;
+        }
+      }
+    }
+    while (wide) {
+      const int i = __ffs(wide) - 1;
+      wide &= wide - 1;
+      atomicAdd(&hist[classify_slow(enc<W>(lds_key<W>(kp, i * THREADS + threadIdx.x), xf), S)], 1u);
     }
     __syncthreads();  // stage st fully consumed before it is refilled
   }
@@ -662,7 +696,8 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
 }
 
 // Scatter: classify again, rank each key within its (warp, child) with a
-// returning shared atomic on a per-warp histogram, scan across warps and
+// returning shared atomic on a per-warp histogram (one atomic per warp when
+// the warp's whole sub-tile falls into one child), scan across warps and
 // children, stage the tile in smem grouped by child (reusing the tile's TMA
 // stage), reserve each child's global range with one atomic per (tile,
 // child), then write each child run with consecutive threads (coalesced).
@@ -677,8 +712,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads) k_scatter(Params<W> P) {
   unsigned short* stage_b = reinterpret_cast<unsigned short*>(smem_raw + kStages * stage_bytes<W>());
   unsigned* whist = reinterpret_cast<unsigned*>(stage_b + TILE);  // [NW][kChildStride]
   __shared__ SplSmem<W> S;
-  __shared__ unsigned toff[kChildStride];
-  __shared__ unsigned long long gbase[kChildStride];
+  __shared__ long long gdelta[kChildStride];  // global index of staged slot 0 of child c
   __shared__ unsigned scan_scratch[32];
   __shared__ __align__(8) unsigned long long bars[kStages];
   __shared__ int s_p;
@@ -726,7 +760,8 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads) k_scatter(Params<W> P) {
     }
     W* dst_buf = P.part_mode ? P.out : ((d.flags & F_IN_B) ? P.a : P.b);
     const int nc = 2 * ((1 << L) - 1) + 1;
-    for (int i = threadIdx.x; i < NW * kChildStride; i += THREADS) whist[i] = 0;
+#pragma unroll
+    for (int i = 0; i < (NW * kChildStride) / THREADS; ++i) whist[i * THREADS + threadIdx.x] = 0;
     const W* src = src_of(P, d.flags);
     const int xf = (d.flags & F_RAW) ? P.xf : XF_NONE;
     const unsigned long long lo = d.start + (t - d.tile_base) * TILE;
@@ -737,34 +772,41 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads) k_scatter(Params<W> P) {
     mbar_wait(&bars[st], (phase >> st) & 1);
     phase ^= 1u << st;
     const unsigned char* kp = tile_fixup<W, THREADS>(src + lo, cnt, span, stage);
-    __syncthreads();
+    __syncthreads();  // tile complete in smem; whist zeroed
     W k[ITEMS];
     int bk[ITEMS];
-    unsigned rk[ITEMS];
+    unsigned wide = 0;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const int idx = i * THREADS + threadIdx.x;
       k[i] = idx < cnt ? enc<W>(lds_key<W>(kp, idx), xf) : key_max<W>();
-      bk[i] = classify(k[i], S);
+      bk[i] = idx < cnt ? classify_fast(k[i], S) : -2;
+      if (bk[i] == -1) wide |= 1u << i;
     }
-    __syncthreads();  // whist zeroed; stage st consumed (reused for staging below)
+    while (wide) {
+      const int i = __ffs(wide) - 1;
+      wide &= wide - 1;
+      bk[i] = classify_slow(k[i], S);
+    }
+    // rank within (warp, child); bk[] becomes child << 16 | rank
+    bool same = bk[0] >= 0;
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const int idx = i * THREADS + threadIdx.x;
-      const bool valid = idx < cnt;
-      if (!valid) bk[i] = -1;
-      const int b0 = __shfl_sync(0xffffffffu, bk[i], 0);
-      const bool uni = __all_sync(0xffffffffu, bk[i] == b0) && b0 >= 0;
-      if (uni) {
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(&myhist[b0], 32u);
-        rk[i] = __shfl_sync(0xffffffffu, base, 0) + lane;
-      } else if (valid) {
-        rk[i] = atomicAdd(&myhist[bk[i]], 1u);
-      }
+    for (int i = 1; i < ITEMS; ++i) same = same && bk[i] == bk[0];
+    const int b0 = __shfl_sync(0xffffffffu, bk[0], 0);
+    if (__all_sync(0xffffffffu, same && bk[0] == b0)) {
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(&myhist[b0], 32u * ITEMS);
+      base = __shfl_sync(0xffffffffu, base, 0) + lane * ITEMS;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) bk[i] = (b0 << 16) | (int)(base + i);
+    } else {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i)
+        if (bk[i] >= 0) bk[i] = (bk[i] << 16) | (int)atomicAdd(&myhist[bk[i]], 1u);
     }
     __syncthreads();
-    // per child: exclusive prefix across warps (in place), then across children
+    // per child: exclusive prefix across warps, then across children; fold
+    // the child's tile offset into each warp's slot
     {
       unsigned tot[PER];
       unsigned sum = 0;
@@ -772,14 +814,8 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads) k_scatter(Params<W> P) {
       for (int j = 0; j < PER; ++j) {
         const int c = threadIdx.x * PER + j;
         unsigned run = 0;
-        if (c < kChildStride) {
 #pragma unroll
-          for (int w = 0; w < NW; ++w) {
-            const unsigned v = whist[w * kChildStride + c];
-            whist[w * kChildStride + c] = run;
-            run += v;
-          }
-        }
+        for (int w = 0; w < NW; ++w) run += whist[w * kChildStride + c];
         tot[j] = run;
         sum += run;
       }
@@ -788,10 +824,17 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads) k_scatter(Params<W> P) {
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
         const int c = threadIdx.x * PER + j;
-        if (c < kChildStride) {
-          toff[c] = ex;
-          if (tot[j] && c < nc)
-            gbase[c] = atomicAdd(P.cursors + (unsigned long long)p * kChildStride + c, (unsigned long long)tot[j]);
+        unsigned run = ex;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const unsigned v = whist[w * kChildStride + c];
+          whist[w * kChildStride + c] = run;
+          run += v;
+        }
+        if (tot[j] && c < nc) {
+          const unsigned long long g =
+              atomicAdd(P.cursors + (unsigned long long)p * kChildStride + c, (unsigned long long)tot[j]);
+          gdelta[c] = (long long)g - (long long)ex;
         }
         ex += tot[j];
       }
@@ -801,15 +844,15 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads) k_scatter(Params<W> P) {
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       if (bk[i] >= 0) {
-        const unsigned pos = toff[bk[i]] + myhist[bk[i]] + rk[i];
+        const int c = bk[i] >> 16;
+        const unsigned pos = myhist[c] + (unsigned)(bk[i] & 0xFFFF);
         staged[pos] = k[i];
-        stage_b[pos] = (unsigned short)bk[i];
+        stage_b[pos] = (unsigned short)c;
       }
     }
     __syncthreads();
     for (int j = threadIdx.x; j < cnt; j += THREADS) {
-      const int c = stage_b[j];
-      const unsigned long long dst = gbase[c] + (unsigned long long)(j - (int)toff[c]);
+      const long long dst = gdelta[stage_b[j]] + j;
       dst_buf[dst] = dec<W>(staged[j], out_xf);
     }
     __syncthreads();
