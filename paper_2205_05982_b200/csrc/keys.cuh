@@ -233,6 +233,32 @@ __host__ __device__ __forceinline__ W dec(W t, int xf) {
   return W(t ^ xf_mask<W>(xf));
 }
 
+// A transform resolved once per kernel/tile: `flt` 0 = integer XOR with
+// `mask`, 1 = float ascending, 2 = float descending.  Hot loops branch on
+// `flt` OUTSIDE the loop (see with_xf) so the per-key cost is one XOR.
+template <typename W>
+struct Xf {
+  W mask;
+  int flt;
+};
+template <typename W>
+__host__ __device__ __forceinline__ Xf<W> make_xf(int xf) {
+  Xf<W> x;
+  x.flt = xf == XF_FLT_ASC ? 1 : (xf == XF_FLT_DESC ? 2 : 0);
+  x.mask = xf_mask<W>(xf);
+  return x;
+}
+template <bool FLT, typename W>
+__host__ __device__ __forceinline__ W enc_x(W b, const Xf<W>& x) {
+  if constexpr (FLT) return flt_enc<W>(b, x.flt == 2);
+  else return W(b ^ x.mask);
+}
+template <bool FLT, typename W>
+__host__ __device__ __forceinline__ W dec_x(W t, const Xf<W>& x) {
+  if constexpr (FLT) return flt_dec<W>(t, x.flt == 2);
+  else return W(t ^ x.mask);
+}
+
 // 16-bit: no float type; only integer transforms.
 template <>
 __host__ __device__ __forceinline__ uint16_t enc<uint16_t>(uint16_t b, int xf) {
@@ -252,6 +278,19 @@ __host__ __device__ __forceinline__ uint16_t dec<uint16_t>(uint16_t t, int xf) {
     default: return t;
   }
 }
+template <>
+__host__ __device__ __forceinline__ uint16_t flt_enc<uint16_t>(uint16_t b, bool) { return b; }
+template <>
+__host__ __device__ __forceinline__ uint16_t flt_dec<uint16_t>(uint16_t t, bool) { return t; }
+template <>
+__host__ __device__ __forceinline__ U128 flt_enc<U128>(U128 b, bool) { return b; }
+template <>
+__host__ __device__ __forceinline__ U128 flt_dec<U128>(U128 t, bool) { return t; }
+template <>
+__host__ __device__ __forceinline__ U128 xf_mask<U128>(int xf) {
+  return xf == XF_NOT ? U128{~0ull, ~0ull} : U128{0, 0};
+}
+__host__ __device__ __forceinline__ U128 operator^(const U128& a, const U128& b) { return U128{a.lo ^ b.lo, a.hi ^ b.hi}; }
 template <>
 __host__ __device__ __forceinline__ U128 enc<U128>(U128 b, int xf) {
   return xf == XF_NOT ? U128{~b.lo, ~b.hi} : b;

@@ -26,6 +26,7 @@
 // that range, so the final base-case/copy pass can always write into A.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "block_sort.cuh"
 #include "keys.cuh"
@@ -70,6 +71,8 @@ struct Cfg {
   static constexpr int kTile = 4096;
   static constexpr int kHistThreads = 256;
   static constexpr int kScatThreads = 256;
+  static constexpr int kScatMinBlocks = 3;
+  static constexpr int kHistMinBlocks = 4;
   static constexpr int kCap = 8192;
 };
 template <>
@@ -77,6 +80,8 @@ struct Cfg<uint16_t> {
   static constexpr int kTile = 8192;
   static constexpr int kHistThreads = 512;
   static constexpr int kScatThreads = 512;
+  static constexpr int kScatMinBlocks = 1;
+  static constexpr int kHistMinBlocks = 2;
   static constexpr int kCap = 8192;
 };
 template <>
@@ -84,6 +89,8 @@ struct Cfg<U128> {
   static constexpr int kTile = 2048;
   static constexpr int kHistThreads = 256;
   static constexpr int kScatThreads = 256;
+  static constexpr int kScatMinBlocks = 2;
+  static constexpr int kHistMinBlocks = 4;
   static constexpr int kCap = 4096;
 };
 constexpr int kStages = 2;  // TMA tile pipeline depth
@@ -222,10 +229,11 @@ constexpr int kLut = 1 << kLutBits;
 
 template <typename W>
 struct SplSmem {
-  W srt[257];  // m splitters + sentinel
+  W srt[257];   // m splitters, padded with the maximum up to 255, + sentinel
+  W tree[256];  // implicit BST over srt[0..254] in BFS order (tree[1..255])
   W lo;
   unsigned cmax;
-  int shift, m;
+  int shift, m, use_tree;
   unsigned short lut[kLut];  // (first, end) splitter index of cell c, packed lo | hi << 8
 };
 
@@ -239,12 +247,25 @@ __device__ __forceinline__ int lower_bound_smem(const W* srt, int lo, int hi, co
   return lo;
 }
 
+// Children of a bucket with m splitters: ids 0..2m+1 (the last one is the
+// equality bucket of the maximum key, used when the tree pads with it).
+__host__ __device__ __forceinline__ int num_children(int L) { return 2 * ((1 << L) - 1) + 2; }
+
+// Load a bucket's splitters, build the lookup table and the tree, and pick
+// the classifier: the table when no cell holds more than 2 splitters for
+// more than a few splitters (uniform-ish key codes), else the 8-level tree
+// (clustered codes, e.g. normal floats or few distinct values).
 template <typename W>
 __device__ __forceinline__ void load_splitters(const W* g_srt, int L, SplSmem<W>& S) {
   __shared__ unsigned char first[kLut + 1];
+  __shared__ int s_wide;
   const int m = (1 << L) - 1;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) S.srt[i] = g_srt[i];
-  if (threadIdx.x == 0) S.srt[m] = key_max<W>();
+  for (int i = threadIdx.x; i < 255; i += blockDim.x) S.srt[i] = i < m ? g_srt[i] : key_max<W>();
+  if (threadIdx.x == 0) {
+    S.srt[255] = key_max<W>();
+    S.srt[256] = key_max<W>();
+    s_wide = 0;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     S.lo = S.srt[0];
@@ -253,6 +274,11 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, int L, SplSmem<W>
     S.shift = bl > kLutBits ? bl - kLutBits : 0;
     S.cmax = key_shr32(range, S.shift);
     S.m = m;
+  }
+  for (int j = threadIdx.x + 1; j < 256; j += blockDim.x) {
+    const int d = 31 - __clz(j);
+    const int q = j - (1 << d);
+    S.tree[j] = S.srt[((2 * q + 1) << (7 - d)) - 1];
   }
   __syncthreads();
   const W lo = S.lo, hi = S.srt[m - 1];
@@ -263,31 +289,55 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, int L, SplSmem<W>
                                                           : (unsigned char)m;
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < kLut; c += blockDim.x)
+  int wide = 0;
+  for (int c = threadIdx.x; c < kLut; c += blockDim.x) {
     S.lut[c] = (unsigned short)(first[c] | ((unsigned)first[c + 1] << 8));
+    const int occ = (int)first[c + 1] - (int)first[c];
+    if (occ > 2) wide += occ;
+  }
+  if (wide) atomicAdd(&s_wide, wide);
+  __syncthreads();
+  if (threadIdx.x == 0) S.use_tree = s_wide > 8 ? 1 : 0;
   __syncthreads();
 }
 
 // Child id of key x: i = #splitters < x (lower bound); an equal splitter sends
 // x to the equality bucket 2i+1, else the normal bucket 2i.  Ids ascend in key
-// order: normal_0 < eq_0 < normal_1 < ... < normal_m.  Keys below the first
-// splitter use cell 0, keys above the last use the last cell; the answer
-// always lies in [first(c), end(c)] and srt[end(c)] >= x (sentinel srt[m] =
-// max), so two unguarded steps finish any cell holding <= 2 splitters.
-// classify_fast returns -1 for the rare wider cells (skewed splitter sets);
-// classify_slow resolves those with a binary search.
+// order: normal_0 < eq_0 < normal_1 < ... < normal_m.
+//
+// Table path: keys below the first splitter use cell 0, keys above the last
+// use the last cell; the answer always lies in [first(c), end(c)] and
+// srt[end(c)] >= x (sentinel), so two unguarded steps finish any cell holding
+// <= 2 splitters; wider cells return -1 for classify_slow.
+// Tree path: branch-free 8-level walk over the padded implicit BST (padding
+// with the maximum key keeps lower-bound semantics; the maximum key itself
+// lands in equality bucket 2m+1).
+template <bool TREE, typename W>
+__device__ __forceinline__ int classify_mode(const W& x, const SplSmem<W>& S) {
+  if constexpr (TREE) {
+    int j = 1;
+#pragma unroll
+    for (int l = 0; l < 8; ++l) j = 2 * j + (key_lt(S.tree[j], x) ? 1 : 0);
+    const int i = j - 256;
+    const int eq = (i < 255 && key_eq(S.srt[i], x)) ? 1 : 0;
+    return 2 * i + eq;
+  } else {
+    unsigned c = key_shr32(key_sub(x, S.lo), S.shift);
+    c = c < S.cmax ? c : S.cmax;
+    c = key_lt(x, S.lo) ? 0u : c;
+    const unsigned pr = S.lut[c];
+    int i = (int)(pr & 0xFFu);
+    const int e = (int)(pr >> 8);
+    i += key_lt(S.srt[i], x) ? 1 : 0;
+    i += key_lt(S.srt[i], x) ? 1 : 0;
+    const int eq = (key_eq(S.srt[i], x) && i < S.m) ? 1 : 0;
+    return e - (int)(pr & 0xFFu) > 2 ? -1 : 2 * i + eq;
+  }
+}
+
 template <typename W>
 __device__ __forceinline__ int classify_fast(const W& x, const SplSmem<W>& S) {
-  unsigned c = key_shr32(key_sub(x, S.lo), S.shift);
-  c = c < S.cmax ? c : S.cmax;
-  c = key_lt(x, S.lo) ? 0u : c;
-  const unsigned pr = S.lut[c];
-  int i = (int)(pr & 0xFFu);
-  const int e = (int)(pr >> 8);
-  i += key_lt(S.srt[i], x) ? 1 : 0;
-  i += key_lt(S.srt[i], x) ? 1 : 0;
-  const int eq = (key_eq(S.srt[i], x) && i < S.m) ? 1 : 0;
-  return e - (int)(pr & 0xFFu) > 2 ? -1 : 2 * i + eq;
+  return S.use_tree ? classify_mode<true>(x, S) : classify_mode<false>(x, S);
 }
 
 template <typename W>
@@ -448,7 +498,7 @@ __host__ __device__ constexpr int stage_bytes() {
 // on B200 with ~500 distinct ids per warp); a warp whose 32 keys share one
 // child (low-entropy input) adds 32 with a single atomic.
 template <typename W>
-__global__ void __launch_bounds__(Cfg<W>::kHistThreads) k_hist(Params<W> P) {
+__global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) k_hist(Params<W> P) {
   constexpr int THREADS = Cfg<W>::kHistThreads;
   constexpr int TILE = Cfg<W>::kTile;
   constexpr int ITEMS = TILE / THREADS;
@@ -492,7 +542,7 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads) k_hist(Params<W> P) {
     }
     if (p + 1 < nb && list[p + 1].tile_base <= t) {
       // flush and move to the next bucket
-      const int nc = 2 * ((1 << L) - 1) + 1;
+      const int nc = num_children(L);
       for (int c = threadIdx.x; c < nc; c += THREADS) {
         if (hist[c]) atomicAdd(P.counts + (unsigned long long)p * kChildStride + c, (unsigned long long)hist[c]);
         hist[c] = 0;
@@ -515,32 +565,44 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads) k_hist(Params<W> P) {
     const unsigned char* kp = tile_fixup<W, THREADS>(src + lo, cnt, span, stage);
     __syncthreads();
     unsigned wide = 0;  // items whose cell holds > 2 splitters (rare)
-    if (cnt == TILE) {
+    const Xf<W> X = make_xf<W>(xf);
+    auto count_tile = [&](auto tree_tag, auto flt_tag) {
+      constexpr bool TREE = decltype(tree_tag)::value;
+      constexpr bool FLT = decltype(flt_tag)::value;
+      if (cnt == TILE) {
 #pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        const int b = classify_fast(enc<W>(lds_key<W>(kp, i * THREADS + threadIdx.x), xf), S);
-        if (b >= 0) atomicAdd(&hist[b], 1u);
-        else wide |= 1u << i;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        const int idx = i * THREADS + threadIdx.x;
-        if (idx < cnt) {
-          const int b = classify_fast(enc<W>(lds_key<W>(kp, idx), xf), S);
+        for (int i = 0; i < ITEMS; ++i) {
+          const int b = classify_mode<TREE>(enc_x<FLT>(lds_key<W>(kp, i * THREADS + threadIdx.x), X), S);
           if (b >= 0) atomicAdd(&hist[b], 1u);
           else wide |= 1u << i;
         }
+      } else {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const int idx = i * THREADS + threadIdx.x;
+          if (idx < cnt) {
+            const int b = classify_mode<TREE>(enc_x<FLT>(lds_key<W>(kp, idx), X), S);
+            if (b >= 0) atomicAdd(&hist[b], 1u);
+            else wide |= 1u << i;
+          }
+        }
       }
+    };
+    if (S.use_tree) {
+      if (X.flt) count_tile(std::true_type{}, std::true_type{});
+      else count_tile(std::true_type{}, std::false_type{});
+    } else {
+      if (X.flt) count_tile(std::false_type{}, std::true_type{});
+      else count_tile(std::false_type{}, std::false_type{});
     }
     while (wide) {
       const int i = __ffs(wide) - 1;
       wide &= wide - 1;
-      atomicAdd(&hist[classify_slow(enc<W>(lds_key<W>(kp, i * THREADS + threadIdx.x), xf), S)], 1u);
+      atomicAdd(&hist[classify_slow(enc<W>(lds_key<W>(kp, i * THREADS + threadIdx.x), xf), S)], 1u);  // rare
     }
     __syncthreads();  // stage st fully consumed before it is refilled
   }
-  const int nc = 2 * ((1 << L) - 1) + 1;
+  const int nc = num_children(L);
   for (int c = threadIdx.x; c < nc; c += THREADS) {
     if (hist[c]) atomicAdd(P.counts + (unsigned long long)p * kChildStride + c, (unsigned long long)hist[c]);
   }
@@ -570,7 +632,7 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
   for (int p = blockIdx.x; p < nb; p += gridDim.x) {
     const SplitDesc d = list[p];
     const int L = (int)d.L;
-    const int nc = 2 * ((1 << L) - 1) + 1;
+    const int nc = num_children(L);
     const int c = threadIdx.x;
     const unsigned long long cnt = c < nc ? P.counts[(unsigned long long)p * kChildStride + c] : 0;
     unsigned long long total;
@@ -702,7 +764,7 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
 // stage), reserve each child's global range with one atomic per (tile,
 // child), then write each child run with consecutive threads (coalesced).
 template <typename W>
-__global__ void __launch_bounds__(Cfg<W>::kScatThreads) k_scatter(Params<W> P) {
+__global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) k_scatter(Params<W> P) {
   constexpr int THREADS = Cfg<W>::kScatThreads;
   constexpr int TILE = Cfg<W>::kTile;
   constexpr int ITEMS = TILE / THREADS;
@@ -759,7 +821,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads) k_scatter(Params<W> P) {
       load_splitters(P.splitters + (unsigned long long)p * 256, L, S);
     }
     W* dst_buf = P.part_mode ? P.out : ((d.flags & F_IN_B) ? P.a : P.b);
-    const int nc = 2 * ((1 << L) - 1) + 1;
+    const int nc = num_children(L);
 #pragma unroll
     for (int i = 0; i < (NW * kChildStride) / THREADS; ++i) whist[i * THREADS + threadIdx.x] = 0;
     const W* src = src_of(P, d.flags);
@@ -776,12 +838,24 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads) k_scatter(Params<W> P) {
     W k[ITEMS];
     int bk[ITEMS];
     unsigned wide = 0;
+    const Xf<W> X = make_xf<W>(xf);
+    auto classify_tile = [&](auto tree_tag, auto flt_tag) {
+      constexpr bool TREE = decltype(tree_tag)::value;
+      constexpr bool FLT = decltype(flt_tag)::value;
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const int idx = i * THREADS + threadIdx.x;
-      k[i] = idx < cnt ? enc<W>(lds_key<W>(kp, idx), xf) : key_max<W>();
-      bk[i] = idx < cnt ? classify_fast(k[i], S) : -2;
-      if (bk[i] == -1) wide |= 1u << i;
+      for (int i = 0; i < ITEMS; ++i) {
+        const int idx = i * THREADS + threadIdx.x;
+        k[i] = idx < cnt ? enc_x<FLT>(lds_key<W>(kp, idx), X) : key_max<W>();
+        bk[i] = idx < cnt ? classify_mode<TREE>(k[i], S) : -2;
+        if (bk[i] == -1) wide |= 1u << i;
+      }
+    };
+    if (S.use_tree) {
+      if (X.flt) classify_tile(std::true_type{}, std::true_type{});
+      else classify_tile(std::true_type{}, std::false_type{});
+    } else {
+      if (X.flt) classify_tile(std::false_type{}, std::true_type{});
+      else classify_tile(std::false_type{}, std::false_type{});
     }
     while (wide) {
       const int i = __ffs(wide) - 1;
@@ -851,9 +925,10 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads) k_scatter(Params<W> P) {
       }
     }
     __syncthreads();
-    for (int j = threadIdx.x; j < cnt; j += THREADS) {
-      const long long dst = gdelta[stage_b[j]] + j;
-      dst_buf[dst] = dec<W>(staged[j], out_xf);
+    if (out_xf == XF_NONE) {
+      for (int j = threadIdx.x; j < cnt; j += THREADS) dst_buf[gdelta[stage_b[j]] + j] = staged[j];
+    } else {  // vxs_partition: decode into the caller's encoding
+      for (int j = threadIdx.x; j < cnt; j += THREADS) dst_buf[gdelta[stage_b[j]] + j] = dec<W>(staged[j], out_xf);
     }
     __syncthreads();
   }
@@ -870,16 +945,24 @@ __global__ void __launch_bounds__(SortClass<CLS>::T) k_final(Params<W> P) {
   W* sm = reinterpret_cast<W*>(smem_raw);
   const unsigned long long nitems = P.ctrl->item_count[CLS];
   const Item* items = P.items[CLS];
+  const Xf<W> X = make_xf<W>(P.xf);
   for (unsigned long long it = blockIdx.x; it < nitems; it += gridDim.x) {
     const Item item = items[it];
     const W* src = (item.flags & F_IN_B) ? P.b : P.a;
-    const int xf = (item.flags & F_RAW) ? P.xf : XF_NONE;
     const int size = (int)item.size;
     W k[ITEMS];
+    if (item.flags & F_RAW) {  // only the root item of a small input is raw
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const int idx = i * THREADS + threadIdx.x;
-      k[i] = idx < size ? enc<W>(ldcs(src + item.start + idx), xf) : key_max<W>();
+      for (int i = 0; i < ITEMS; ++i) {
+        const int idx = i * THREADS + threadIdx.x;
+        k[i] = idx < size ? enc<W>(ldcs(src + item.start + idx), P.xf) : key_max<W>();
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int idx = i * THREADS + threadIdx.x;
+        k[i] = idx < size ? ldcs(src + item.start + idx) : key_max<W>();
+      }
     }
     // 32-bit and narrower keys merge inside the warp with __shfl_xor_sync
     // networks (measured faster); 64/128-bit keys use shared-memory merge path.
@@ -889,7 +972,11 @@ __global__ void __launch_bounds__(SortClass<CLS>::T) k_final(Params<W> P) {
     for (int i = 0; i < ITEMS; ++i) sm[pad_idx<W>(threadIdx.x * ITEMS + i)] = k[i];
     __syncthreads();
     W* dst = P.a + item.start;
-    for (int idx = threadIdx.x; idx < size; idx += THREADS) dst[idx] = dec<W>(sm[pad_idx<W>(idx)], P.xf);
+    if (X.flt) {
+      for (int idx = threadIdx.x; idx < size; idx += THREADS) dst[idx] = dec_x<true>(sm[pad_idx<W>(idx)], X);
+    } else {
+      for (int idx = threadIdx.x; idx < size; idx += THREADS) dst[idx] = dec_x<false>(sm[pad_idx<W>(idx)], X);
+    }
     __syncthreads();
   }
   (void)TOTAL;
