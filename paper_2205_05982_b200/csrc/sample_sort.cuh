@@ -437,21 +437,21 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
       }
     }
     __syncthreads();
-    // bitonic sort of S (power of two) keys in smem
-    for (int size = 2; size <= S; size <<= 1) {
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        for (int i = threadIdx.x; i < S / 2; i += THREADS) {
-          const int lo_i = 2 * i - (i & (stride - 1));
-          const int hi_i = lo_i + stride;
-          W x = s[lo_i], y = s[hi_i];
-          const bool up = (lo_i & size) == 0;
-          if (up ? key_lt(y, x) : key_lt(x, y)) {
-            s[lo_i] = y;
-            s[hi_i] = x;
-          }
-        }
-        __syncthreads();
+    // sort the S samples (padded to 4096 with the maximum) with the block
+    // base-case sort, 512 threads x 8 keys, then stage them back to smem
+    {
+      constexpr int SI = kMaxSamples / THREADS;
+      W k[SI];
+#pragma unroll
+      for (int i = 0; i < SI; ++i) {
+        const int idx = i * THREADS + threadIdx.x;
+        k[i] = idx < S ? s[idx] : key_max<W>();
       }
+      __syncthreads();
+      block_sort<W, THREADS, SI, sizeof(W) <= 4>(k, s);
+#pragma unroll
+      for (int i = 0; i < SI; ++i) s[threadIdx.x * SI + i] = k[i];
+      __syncthreads();
     }
     W* g = P.splitters + (unsigned long long)p * 256;
     const int step = S / (m + 1);
@@ -618,13 +618,12 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
   __shared__ unsigned long long s_cnt[kChildStride];
   __shared__ unsigned long long s_off[kChildStride];
   __shared__ unsigned long long scan_scratch[32];
-  // grouped items built by thread 0
-  __shared__ unsigned long long g_start[kChildStride + 8];
-  __shared__ unsigned long long g_size[kChildStride + 8];
-  __shared__ int g_list[kChildStride + 8];
-  __shared__ int s_ng;
+  __shared__ unsigned char s_kind[kChildStride];
   __shared__ unsigned long long s_res[kNumLists];
+  __shared__ unsigned long long s_base[kNumLists];
+  __shared__ unsigned long long s_nsort;
   __shared__ unsigned long long s_split_base;
+  if (threadIdx.x == 0) s_nsort = 0;
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
   const int nb = (int)(packed >> 40);
   const SplitDesc* list = P.split[P.cur];
@@ -668,89 +667,77 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
         P.ctrl->error = 1;
       }
     }
-    // group the remaining children (sequential, smem only)
-    if (c == 0) {
-      int ng = 0;
-      unsigned long long gs = 0, gz = 0;
-      bool gsort = false;
-      const bool need_copy = (child_flags & F_IN_B) || P.xf != XF_NONE;
-      auto emit = [&]() {
-        if (gz == 0) return;
-        int lst;
-        if (gsort) lst = class_for(gz);
-        else lst = need_copy ? kListCopySmall : -1;
-        if (lst >= 0) {
-          g_start[ng] = gs;
-          g_size[ng] = gz;
-          g_list[ng] = lst;
-          ++ng;
-        }
-        gz = 0;
-        gsort = false;
-      };
-      for (int ch = 0; ch < nc; ++ch) {
-        const unsigned long long s = s_cnt[ch];
-        if (s == 0) continue;
-        const bool eq = (ch & 1) != 0;
-        if (!eq && s > CAP) {  // split child
-          emit();
-          continue;
-        }
-        if (eq && s > CAP) {  // big equality bucket: one cooperative copy item
-          emit();
-          if (need_copy) {
-            g_start[ng] = d.start + s_off[ch];
-            g_size[ng] = s;
-            g_list[ng] = kListCopyBig;
-            ++ng;
-          }
-          continue;
-        }
-        if (gz + s > CAP || gz >= kGroupTarget) emit();
-        if (gz == 0) gs = d.start + s_off[ch];
-        gz += s;
-        gsort = gsort || (!eq && s > 1);
+    // Group the remaining children in parallel.  Kinds: SPLIT (handled
+    // above), BIGEQ (equality bucket > Cap: one cooperative copy item), SOLO
+    // (>= kGroupTarget keys: its own item), SMALL (< kGroupTarget, incl.
+    // empty).  Consecutive SMALL children whose parent-relative start offsets
+    // fall in the same kGroupTarget window form one item (< 2*kGroupTarget
+    // <= Cap keys), so a group never needs a sequential greedy pass.
+    const bool eqc = (c & 1) != 0;
+    const bool small = c < nc && cnt < kGroupTarget;
+    s_kind[c] = c >= nc ? 0 : (small ? 1 : 2);  // 0 none, 1 small, 2 other
+    __syncthreads();
+    const bool need_copy = (child_flags & F_IN_B) || P.xf != XF_NONE;
+    int my_list = -1;
+    unsigned long long my_start = 0, my_size = 0;
+    if (c < nc && !small) {
+      if (!eqc && cnt > CAP) {
+        // split child: already queued
+      } else if (eqc && cnt > CAP) {
+        if (need_copy) my_list = kListCopyBig;
+      } else {
+        my_list = (!eqc && cnt > 1) ? class_for(cnt) : (need_copy ? kListCopySmall : -1);
       }
-      emit();
-      s_ng = ng;
-      for (int l = 0; l < kNumLists; ++l) s_res[l] = 0;
-      for (int g = 0; g < ng; ++g) s_res[g_list[g]] += 1;
-      unsigned long long nsort = 0;
-      for (int l = 0; l < kNumLists; ++l) {
-        const unsigned long long k = s_res[l];
-        if (l < kNumSortClasses) nsort += k;
-        s_res[l] = k ? atomicAdd(&P.ctrl->item_count[l], k) : 0;
+      my_start = d.start + off;
+      my_size = cnt;
+    } else if (small) {
+      const unsigned long long win = off / kGroupTarget;
+      const bool leader = c == 0 || s_kind[c - 1] != 1 || (s_off[c - 1] / kGroupTarget) != win;
+      if (leader) {
+        unsigned long long gz = 0;
+        bool gsort = false;
+        for (int e = c; e < nc && s_kind[e] == 1 && (s_off[e] / kGroupTarget) == win; ++e) {
+          gz += s_cnt[e];
+          gsort = gsort || ((e & 1) == 0 && s_cnt[e] > 1);
+        }
+        if (gz) {
+          my_list = gsort ? class_for(gz) : (need_copy ? kListCopySmall : -1);
+          my_start = d.start + off;
+          my_size = gz;
+        }
       }
+    }
+    if (c < kNumLists) s_res[c] = 0;
+    __syncthreads();
+    unsigned long long my_slot = 0;
+    if (my_list >= 0) my_slot = atomicAdd(&s_res[my_list], 1ull);
+    __syncthreads();
+    if (c < kNumLists) {
+      const unsigned long long k = s_res[c];
+      s_base[c] = k ? atomicAdd(&P.ctrl->item_count[c], k) : 0;
+      if (c < kNumSortClasses && k) atomicAdd(&s_nsort, k);
+    }
+    if (c == 32) {
       atomicAdd(&P.ctrl->partition_calls, 1ull);
       atomicAdd(&P.ctrl->keys_partitioned, d.size);
-      if (nsort) atomicAdd(&P.ctrl->base_cases, nsort);
     }
     __syncthreads();
-    if (c < 32) {
-      // write items: warp 0, in order per list (rank among same-list items)
-      const int ng = s_ng;
-      for (int g0 = 0; g0 < ng; g0 += 32) {
-        const int g = g0 + c;
-        int lst = g < ng ? g_list[g] : -1;
-        // rank of this group among earlier groups of the same list
-        unsigned long long rank = 0;
-        for (int h = 0; h < g0; ++h) rank += (g_list[h] == lst);
-        const unsigned same = __match_any_sync(0xffffffffu, lst);
-        rank += __popc(same & lanemask_lt());
-        if (g < ng) {
-          const unsigned long long slot = s_res[lst] + rank;
-          if (slot < P.cap_items) {
-            Item it;
-            it.start = g_start[g];
-            it.size = g_size[g];
-            it.flags = child_flags;
-            it.pad = 0;
-            it.pad2 = 0;
-            P.items[lst][slot] = it;
-          } else {
-            P.ctrl->error = 2;
-          }
-        }
+    if (c == 0 && s_nsort) {
+      atomicAdd(&P.ctrl->base_cases, s_nsort);
+      s_nsort = 0;
+    }
+    if (my_list >= 0) {
+      const unsigned long long slot = s_base[my_list] + my_slot;
+      if (slot < P.cap_items) {
+        Item it;
+        it.start = my_start;
+        it.size = my_size;
+        it.flags = child_flags;
+        it.pad = 0;
+        it.pad2 = 0;
+        P.items[my_list][slot] = it;
+      } else {
+        P.ctrl->error = 2;
       }
     }
     __syncthreads();

@@ -174,7 +174,7 @@ Params<W> make_params(W* keys, size_t n, int xf, uint64_t seed, unsigned char* w
 
 template <typename W>
 constexpr size_t sample_smem() {
-  return kMaxSamples * sizeof(W);
+  return (size_t)padded_size<W>(kMaxSamples) * sizeof(W);
 }
 template <typename W>
 constexpr size_t hist_smem() {
