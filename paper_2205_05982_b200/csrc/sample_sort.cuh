@@ -224,7 +224,7 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* total, T* scratch /*[3
 // lut[c+1]], so typical keys need one table load and 0-1 splitter
 // comparisons instead of an 8-level tree walk (binary search inside the
 // cell keeps skewed splitter sets exact and O(log)).
-constexpr int kLutBits = 11;
+constexpr int kLutBits = 12;
 constexpr int kLut = 1 << kLutBits;
 
 template <typename W>
@@ -293,7 +293,7 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, int L, SplSmem<W>
   for (int c = threadIdx.x; c < kLut; c += blockDim.x) {
     S.lut[c] = (unsigned short)(first[c] | ((unsigned)first[c + 1] << 8));
     const int occ = (int)first[c + 1] - (int)first[c];
-    if (occ > 2) wide += occ;
+    if (occ > 1) wide += occ;
   }
   if (wide) atomicAdd(&s_wide, wide);
   __syncthreads();
@@ -322,16 +322,20 @@ __device__ __forceinline__ int classify_mode(const W& x, const SplSmem<W>& S) {
     const int eq = (i < 255 && key_eq(S.srt[i], x)) ? 1 : 0;
     return 2 * i + eq;
   } else {
+    // Cell c holds splitters [i, e).  e == i: answer i, no equality possible
+    // (srt[i] >= end of cell > x).  e == i+1: one compare with srt[i] gives
+    // the answer and the equality bit.  Wider cells take the slow path.
     unsigned c = key_shr32(key_sub(x, S.lo), S.shift);
     c = c < S.cmax ? c : S.cmax;
     c = key_lt(x, S.lo) ? 0u : c;
     const unsigned pr = S.lut[c];
-    int i = (int)(pr & 0xFFu);
+    const int i = (int)(pr & 0xFFu);
     const int e = (int)(pr >> 8);
-    i += key_lt(S.srt[i], x) ? 1 : 0;
-    i += key_lt(S.srt[i], x) ? 1 : 0;
-    const int eq = (key_eq(S.srt[i], x) && i < S.m) ? 1 : 0;
-    return e - (int)(pr & 0xFFu) > 2 ? -1 : 2 * i + eq;
+    const W sp = S.srt[i];
+    const bool has = e > i;
+    const bool lt = has && key_lt(sp, x);
+    const bool eq = has && !lt && key_eq(sp, x);
+    return e - i > 1 ? -1 : 2 * (i + (lt ? 1 : 0)) + (eq ? 1 : 0);
   }
 }
 
