@@ -232,7 +232,10 @@ vxs_status launch_level(Params<W>& P, cudaStream_t st, int& launches) {
 template <typename W, int CLS>
 void launch_final(Params<W>& P, unsigned long long count, cudaStream_t st) {
   constexpr int T = SortClass<CLS>::T;
-  constexpr size_t smem = (size_t)padded_size<W>(T * SortClass<CLS>::I) * sizeof(W);
+  constexpr int TOT = T * SortClass<CLS>::I;
+  constexpr size_t smem_a = (size_t)padded_size<W>(TOT) * sizeof(W);
+  constexpr size_t smem_b = (size_t)TOT * sizeof(W) + (size_t)padded_size<unsigned>(TOT) * sizeof(unsigned);
+  constexpr size_t smem = smem_a > smem_b ? smem_a : smem_b;
   ProfScope ps(K_FINAL0 + CLS, st);
   auto fn = k_final<W, CLS>;
   int g = grid_for((const void*)fn, T, smem);
