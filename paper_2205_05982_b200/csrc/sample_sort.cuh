@@ -39,7 +39,8 @@ constexpr int kChildStride = 512;   // child slots per split bucket (2*255+1 use
 constexpr int kNumSortClasses = 5;  // base-case size classes
 constexpr int kListCopySmall = kNumSortClasses;
 constexpr int kListCopyBig = kNumSortClasses + 1;
-constexpr int kNumLists = kNumSortClasses + 2;
+constexpr int kListFallback = kNumSortClasses + 2;  // >= 8-byte items the prefix sort rejected
+constexpr int kNumLists = kNumSortClasses + 3;
 constexpr int kMaxSamples = 4096;
 constexpr unsigned long long kTileMask = (1ull << 40) - 1;
 
@@ -1071,20 +1072,61 @@ __global__ void __launch_bounds__(SortClass<CLS>::T) k_final(Params<W> P) {
     }
     W* dst = P.a + item.start;
     if constexpr (sizeof(W) >= 8 && THREADS * ITEMS >= 512) {
-      if (prefix_sort_item<W, THREADS, ITEMS>(k, size, smem_raw, dst, X)) continue;
+      // keys of 8+ bytes: prefix-compressed sort; rejected items (clustered
+      // keys) go to the full-width fallback kernel, keeping this one lean
+      if (!prefix_sort_item<W, THREADS, ITEMS>(k, size, smem_raw, dst, X) && threadIdx.x == 0) {
+        const unsigned long long slot = atomicAdd(&P.ctrl->item_count[kListFallback], 1ull);
+        if (slot < P.cap_items) P.items[kListFallback][slot] = item;
+        else P.ctrl->error = 3;
+      }
+      __syncthreads();
+    } else {
+      // 32-bit and narrower keys merge inside the warp with __shfl_xor_sync
+      // networks (measured faster); 64/128-bit keys use shared-memory merge path.
+      constexpr bool kWN = SortClass<CLS>::kWarpNet || sizeof(W) <= 4;
+      block_sort<W, THREADS, ITEMS, kWN>(k, sm);
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) sm[pad_idx<W>(threadIdx.x * ITEMS + i)] = k[i];
+      __syncthreads();
+      if (X.flt) {
+        for (int idx = threadIdx.x; idx < size; idx += THREADS) dst[idx] = dec_x<true>(sm[pad_idx<W>(idx)], X);
+      } else {
+        for (int idx = threadIdx.x; idx < size; idx += THREADS) dst[idx] = dec_x<false>(sm[pad_idx<W>(idx)], X);
+      }
+      __syncthreads();
     }
-    // 32-bit and narrower keys merge inside the warp with __shfl_xor_sync
-    // networks (measured faster); 64/128-bit keys use shared-memory merge path.
-    constexpr bool kWN = SortClass<CLS>::kWarpNet || sizeof(W) <= 4;
-    block_sort<W, THREADS, ITEMS, kWN>(k, sm);
+  }
+}
+
+// Full-width merge sort of the items the prefix-compressed sort rejected
+// (persistent; reads the fallback count on the device, usually zero).
+template <typename W>
+__global__ void __launch_bounds__(SortClass<4>::T) k_final_fallback(Params<W> P) {
+  constexpr int THREADS = SortClass<4>::T;
+  constexpr int ITEMS = (sizeof(W) >= 16) ? 8 : 16;  // capacity >= Cap
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  W* sm = reinterpret_cast<W*>(smem_raw);
+  const unsigned long long nitems = P.ctrl->item_count[kListFallback];
+  const Item* items = P.items[kListFallback];
+  const Xf<W> X = make_xf<W>(P.xf);
+  for (unsigned long long it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const Item item = items[it];
+    const W* src = (item.flags & F_IN_B) ? P.b : P.a;
+    const int size = (int)item.size;
+    W k[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * THREADS + threadIdx.x;
+      k[i] = idx < size ? ((item.flags & F_RAW) ? enc<W>(ldcs(src + item.start + idx), P.xf)
+                                                : ldcs(src + item.start + idx))
+                        : key_max<W>();
+    }
+    block_sort<W, THREADS, ITEMS, false>(k, sm);
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) sm[pad_idx<W>(threadIdx.x * ITEMS + i)] = k[i];
     __syncthreads();
-    if (X.flt) {
-      for (int idx = threadIdx.x; idx < size; idx += THREADS) dst[idx] = dec_x<true>(sm[pad_idx<W>(idx)], X);
-    } else {
-      for (int idx = threadIdx.x; idx < size; idx += THREADS) dst[idx] = dec_x<false>(sm[pad_idx<W>(idx)], X);
-    }
+    W* dst = P.a + item.start;
+    for (int idx = threadIdx.x; idx < size; idx += THREADS) dst[idx] = dec<W>(sm[pad_idx<W>(idx)], P.xf);
     __syncthreads();
   }
 }

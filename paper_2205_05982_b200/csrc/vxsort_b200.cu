@@ -44,11 +44,11 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // ---- optional per-kernel event timing (measurement tools only) -----------
 enum KernelId : int {
   K_INIT = 0, K_SAMPLE, K_HIST, K_PLAN, K_SCATTER, K_FINAL0, K_FINAL1, K_FINAL2, K_FINAL3, K_FINAL4,
-  K_COPY, K_PART, K_MISC, K_COUNT
+  K_FALLBACK, K_COPY, K_PART, K_MISC, K_COUNT
 };
 const char* kKernelNames[K_COUNT] = {"k_init", "k_sample", "k_hist", "k_plan", "k_scatter", "k_final_c0",
-                                     "k_final_c1", "k_final_c2", "k_final_c3", "k_final_c4", "k_copy",
-                                     "k_part", "k_misc"};
+                                     "k_final_c1", "k_final_c2", "k_final_c3", "k_final_c4",
+                                     "k_final_fallback", "k_copy", "k_part", "k_misc"};
 struct Prof {
   bool on = false;
   std::mutex mu;
@@ -282,7 +282,7 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
       }
       VXS_CK(cudaMemcpyAsync(&h, P.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st), "ctrl readback");
       VXS_CK(cudaStreamSynchronize(st), "level sync");
-      if (h.error) {
+      if (h.error) {  // (final-phase overflow is checked by the error flag below)
         if (owned) cudaFreeAsync(owned, st);
         return fail(VXS_INTERNAL, "vxsort_b200: device scheduler list overflow");
       }
@@ -304,6 +304,18 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
   if (h.item_count[3]) { launch_final<W, 3>(P, h.item_count[3], st); ++launches; }
   if constexpr (Cfg<W>::kCap >= 8192) {
     if (h.item_count[4]) { launch_final<W, 4>(P, h.item_count[4], st); ++launches; }
+  }
+  if constexpr (sizeof(W) >= 8) {
+    // items rejected by the prefix-compressed base case (count lives on the device)
+    if (h.item_count[0] + h.item_count[1] + h.item_count[2] + h.item_count[3] + h.item_count[4]) {
+      ProfScope ps(K_FALLBACK, st);
+      constexpr int ITEMS = sizeof(W) >= 16 ? 8 : 16;
+      constexpr size_t smem = (size_t)padded_size<W>(SortClass<4>::T * ITEMS) * sizeof(W);
+      auto fn = k_final_fallback<W>;
+      const int g = grid_for((const void*)fn, SortClass<4>::T, smem);
+      fn<<<g, SortClass<4>::T, smem, st>>>(P);
+      ++launches;
+    }
   }
   if (h.item_count[kListCopySmall] || h.item_count[kListCopyBig]) {
     ProfScope ps(K_COPY, st);
