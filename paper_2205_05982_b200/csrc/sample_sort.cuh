@@ -72,6 +72,7 @@ struct Cfg {
   static constexpr int kTile = 4096;
   static constexpr int kHistThreads = 256;
   static constexpr int kScatThreads = 256;
+  static constexpr int kHistCopies = 1;
   static constexpr int kScatMinBlocks = 3;
   static constexpr int kHistMinBlocks = 4;
   static constexpr int kCap = 8192;
@@ -81,6 +82,7 @@ struct Cfg<uint16_t> {
   static constexpr int kTile = 8192;
   static constexpr int kHistThreads = 512;
   static constexpr int kScatThreads = 512;
+  static constexpr int kHistCopies = 1;
   static constexpr int kScatMinBlocks = 1;
   static constexpr int kHistMinBlocks = 2;
   static constexpr int kCap = 8192;
@@ -90,6 +92,7 @@ struct Cfg<U128> {
   static constexpr int kTile = 2048;
   static constexpr int kHistThreads = 256;
   static constexpr int kScatThreads = 256;
+  static constexpr int kHistCopies = 1;
   static constexpr int kScatMinBlocks = 2;
   static constexpr int kHistMinBlocks = 4;
   static constexpr int kCap = 4096;
@@ -764,7 +767,8 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   constexpr int PER = kChildStride / THREADS > 0 ? kChildStride / THREADS : 1;  // children per thread
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned short* stage_b = reinterpret_cast<unsigned short*>(smem_raw + kStages * stage_bytes<W>());
-  unsigned* whist = reinterpret_cast<unsigned*>(stage_b + TILE);  // [NW][kChildStride]
+  constexpr int HC = Cfg<W>::kHistCopies;  // histogram copies (warp w uses copy w % HC)
+  unsigned* whist = reinterpret_cast<unsigned*>(stage_b + TILE);  // [HC][kChildStride]
   __shared__ SplSmem<W> S;
   __shared__ long long gdelta[kChildStride];  // global index of staged slot 0 of child c
   __shared__ unsigned scan_scratch[32];
@@ -795,7 +799,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   load_splitters(P.splitters + (unsigned long long)p * 256, L, S);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  unsigned* myhist = whist + warp * kChildStride;
+  unsigned* myhist = whist + (warp % HC) * kChildStride;
   const int out_xf = P.part_mode ? P.xf : XF_NONE;
   unsigned phase = 0;
   for (unsigned long long t = t0; t < t1; ++t) {
@@ -815,7 +819,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     W* dst_buf = P.part_mode ? P.out : ((d.flags & F_IN_B) ? P.a : P.b);
     const int nc = num_children(L);
 #pragma unroll
-    for (int i = 0; i < (NW * kChildStride) / THREADS; ++i) whist[i * THREADS + threadIdx.x] = 0;
+    for (int i = threadIdx.x; i < HC * kChildStride; i += THREADS) whist[i] = 0;
     const W* src = src_of(P, d.flags);
     const int xf = (d.flags & F_RAW) ? P.xf : XF_NONE;
     const unsigned long long lo = d.start + (t - d.tile_base) * TILE;
@@ -881,7 +885,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
         const int c = threadIdx.x * PER + j;
         unsigned run = 0;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) run += whist[w * kChildStride + c];
+        for (int w = 0; w < HC; ++w) run += whist[w * kChildStride + c];
         tot[j] = run;
         sum += run;
       }
@@ -892,7 +896,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
         const int c = threadIdx.x * PER + j;
         unsigned run = ex;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) {
+        for (int w = 0; w < HC; ++w) {
           const unsigned v = whist[w * kChildStride + c];
           whist[w * kChildStride + c] = run;
           run += v;

@@ -183,7 +183,7 @@ constexpr size_t hist_smem() {
 template <typename W>
 constexpr size_t scatter_smem() {
   return (size_t)kStages * stage_bytes<W>() + (size_t)Cfg<W>::kTile * sizeof(unsigned short) +
-         (size_t)(Cfg<W>::kScatThreads / 32) * kChildStride * sizeof(unsigned);
+         (size_t)Cfg<W>::kHistCopies * kChildStride * sizeof(unsigned);
 }
 
 // Levels a uniform input of n keys needs (>=128-way shrink per level).
