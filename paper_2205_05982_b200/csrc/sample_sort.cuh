@@ -78,6 +78,16 @@ struct Cfg {
   static constexpr int kCap = 8192;
 };
 template <>
+struct Cfg<unsigned long long> {
+  static constexpr int kTile = 2048;
+  static constexpr int kHistThreads = 256;
+  static constexpr int kScatThreads = 256;
+  static constexpr int kHistCopies = 1;
+  static constexpr int kScatMinBlocks = 3;
+  static constexpr int kHistMinBlocks = 4;
+  static constexpr int kCap = 8192;
+};
+template <>
 struct Cfg<uint16_t> {
   static constexpr int kTile = 8192;
   static constexpr int kHistThreads = 512;
@@ -763,7 +773,6 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   constexpr int THREADS = Cfg<W>::kScatThreads;
   constexpr int TILE = Cfg<W>::kTile;
   constexpr int ITEMS = TILE / THREADS;
-  constexpr int NW = THREADS / 32;
   constexpr int PER = kChildStride / THREADS > 0 ? kChildStride / THREADS : 1;  // children per thread
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned short* stage_b = reinterpret_cast<unsigned short*>(smem_raw + kStages * stage_bytes<W>());
