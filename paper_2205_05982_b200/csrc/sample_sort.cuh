@@ -73,8 +73,8 @@ struct Cfg {
   static constexpr int kHistThreads = 256;
   static constexpr int kScatThreads = 256;
   static constexpr int kHistCopies = 1;
-  static constexpr int kScatMinBlocks = 3;
-  static constexpr int kHistMinBlocks = 4;
+  static constexpr int kScatMinBlocks = 4;
+  static constexpr int kHistMinBlocks = 5;
   static constexpr int kCap = 8192;
 };
 template <>
@@ -83,8 +83,8 @@ struct Cfg<unsigned long long> {
   static constexpr int kHistThreads = 256;
   static constexpr int kScatThreads = 256;
   static constexpr int kHistCopies = 1;
-  static constexpr int kScatMinBlocks = 3;
-  static constexpr int kHistMinBlocks = 4;
+  static constexpr int kScatMinBlocks = 4;
+  static constexpr int kHistMinBlocks = 5;
   static constexpr int kCap = 8192;
 };
 template <>

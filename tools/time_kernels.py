@@ -1,0 +1,42 @@
+"""Per-kernel device times of one workload (no validation; for experiments).
+    python tools/time_kernels.py --workload c2-u32-asc --reps 5"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2205_05982_b200 as vx  # noqa: E402
+from paper_2205_05982_b200 import workloads  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="c2-u32-asc")
+ap.add_argument("--n", type=int, default=None)
+ap.add_argument("--reps", type=int, default=5)
+a = ap.parse_args()
+x, kt, desc = workloads.make(a.workload, n=a.n)
+src = torch.from_numpy(x).cuda()
+buf = torch.empty_like(src)
+ws = torch.empty(vx.workspace_bytes(x.shape[0], kt), dtype=torch.uint8, device="cuda")
+cfg = vx.SortConfig(order=vx.Order(int(desc)), seed=1)
+ktarg = kt if kt in ("k128", "kv64") else None
+for _ in range(2):
+    buf.copy_(src)
+    vx.sort(buf, cfg, key_type=ktarg, workspace=ws)
+torch.cuda.synchronize()
+vx.profile_reset()
+vx.profile_enable(True)
+ev = []
+for _ in range(a.reps):
+    buf.copy_(src)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    vx.sort(buf, cfg, key_type=ktarg, workspace=ws)
+    e.record()
+    torch.cuda.synchronize()
+    ev.append(s.elapsed_time(e))
+prof = vx.profile_read()
+print(a.workload, "ms/sort", round(sum(ev) / len(ev), 4),
+      {k: round(v[1] / a.reps, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])})
