@@ -281,6 +281,13 @@ def e2e_host(x, kt, desc, steps):
 
 def roofline(prof, stats, n, kb, peak):
     bytes_ = algorithmic_bytes(stats, n, kb)
+    agg = {}
+    for name, (l, ms) in prof.items():  # per-level entries "k_scatter@L0" -> "k_scatter"
+        base = name.split("@")[0]
+        a = agg.setdefault(base, [0, 0.0])
+        a[0] += l
+        a[1] += ms
+    prof = {k: tuple(v) for k, v in agg.items()}
     fin_l = sum(v[0] for k, v in prof.items() if k.startswith("k_final"))
     fin_ms = sum(v[1] for k, v in prof.items() if k.startswith("k_final"))
     per_kernel = {}

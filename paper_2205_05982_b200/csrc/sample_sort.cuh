@@ -900,6 +900,10 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       }
       unsigned total;
       unsigned ex = block_exclusive_scan<THREADS>(sum, &total, scan_scratch);
+      // reserve each child's global range now, consume the result only after
+      // staging so the atomic round trip overlaps the smem work
+      unsigned long long gres[PER];
+      unsigned exc[PER];
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
         const int c = threadIdx.x * PER + j;
@@ -910,25 +914,30 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
           whist[w * kChildStride + c] = run;
           run += v;
         }
-        if (tot[j] && c < nc) {
-          const unsigned long long g =
-              atomicAdd(P.cursors + (unsigned long long)p * kChildStride + c, (unsigned long long)tot[j]);
-          gdelta[c] = (long long)g - (long long)ex;
-        }
+        gres[j] = (tot[j] && c < nc)
+                      ? atomicAdd(P.cursors + (unsigned long long)p * kChildStride + c, (unsigned long long)tot[j])
+                      : 0ull;
+        exc[j] = ex;
         ex += tot[j];
       }
-    }
-    __syncthreads();
-    W* staged = reinterpret_cast<W*>(stage);
+      __syncthreads();
+      W* staged = reinterpret_cast<W*>(stage);
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      if (bk[i] >= 0) {
-        const int c = bk[i] >> 16;
-        const unsigned pos = myhist[c] + (unsigned)(bk[i] & 0xFFFF);
-        staged[pos] = k[i];
-        stage_b[pos] = (unsigned short)c;
+      for (int i = 0; i < ITEMS; ++i) {
+        if (bk[i] >= 0) {
+          const int c = bk[i] >> 16;
+          const unsigned pos = myhist[c] + (unsigned)(bk[i] & 0xFFFF);
+          staged[pos] = k[i];
+          stage_b[pos] = (unsigned short)c;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int c = threadIdx.x * PER + j;
+        if (tot[j] && c < nc) gdelta[c] = (long long)gres[j] - (long long)exc[j];
       }
     }
+    W* staged = reinterpret_cast<W*>(stage);
     __syncthreads();
     if (out_xf == XF_NONE) {
       for (int j = threadIdx.x; j < cnt; j += THREADS) dst_buf[gdelta[stage_b[j]] + j] = staged[j];

@@ -55,8 +55,10 @@ struct Prof {
   struct Rec { int id; cudaEvent_t a, b; };
   std::vector<Rec> pending;
   std::vector<cudaEvent_t> pool;
-  double ms[K_COUNT] = {};
-  long long launches[K_COUNT] = {};
+  // slot = kernel id + K_COUNT * (level + 1) for per-level kernels
+  static constexpr int kSlots = K_COUNT * 9;
+  double ms[kSlots] = {};
+  long long launches[kSlots] = {};
 } g_prof;
 
 cudaEvent_t prof_event() {
@@ -201,25 +203,25 @@ template <typename W>
 vxs_status launch_level(Params<W>& P, cudaStream_t st, int& launches) {
   constexpr int kSampleThreads = 512;
   {
-    ProfScope ps(K_SAMPLE, st);
+    ProfScope ps(K_SAMPLE + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
     auto fn = k_sample<W, kSampleThreads>;
     const int g = grid_for((const void*)fn, kSampleThreads, sample_smem<W>());
     fn<<<g, kSampleThreads, sample_smem<W>(), st>>>(P);
   }
   {
-    ProfScope ps(K_HIST, st);
+    ProfScope ps(K_HIST + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
     auto fn = k_hist<W>;
     const int g = grid_for((const void*)fn, Cfg<W>::kHistThreads, hist_smem<W>());
     fn<<<g, Cfg<W>::kHistThreads, hist_smem<W>(), st>>>(P);
   }
   {
-    ProfScope ps(K_PLAN, st);
+    ProfScope ps(K_PLAN + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
     auto fn = k_plan<W>;
     const int g = grid_for((const void*)fn, kChildStride, 0);
     fn<<<g, kChildStride, 0, st>>>(P);
   }
   {
-    ProfScope ps(K_SCATTER, st);
+    ProfScope ps(K_SCATTER + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
     auto fn = k_scatter<W>;
     const int g = grid_for((const void*)fn, Cfg<W>::kScatThreads, scatter_smem<W>());
     fn<<<g, Cfg<W>::kScatThreads, scatter_smem<W>(), st>>>(P);
@@ -408,7 +410,7 @@ void vxs_profile_reset(void) {
     g_prof.pool.push_back(r.b);
   }
   g_prof.pending.clear();
-  for (int i = 0; i < K_COUNT; ++i) {
+  for (int i = 0; i < Prof::kSlots; ++i) {
     g_prof.ms[i] = 0;
     g_prof.launches[i] = 0;
   }
@@ -427,9 +429,11 @@ int vxs_profile_read(vxs_kernel_profile* out, int cap) {
   }
   g_prof.pending.clear();
   int k = 0;
-  for (int i = 0; i < K_COUNT && k < cap; ++i) {
+  for (int i = 0; i < Prof::kSlots && k < cap; ++i) {
     if (!g_prof.launches[i]) continue;
-    std::snprintf(out[k].name, sizeof(out[k].name), "%s", kKernelNames[i]);
+    const int kid = i % K_COUNT, lv = i / K_COUNT;
+    if (lv == 0) std::snprintf(out[k].name, sizeof(out[k].name), "%s", kKernelNames[kid]);
+    else std::snprintf(out[k].name, sizeof(out[k].name), "%s@L%d", kKernelNames[kid], lv - 1);
     out[k].launches = g_prof.launches[i];
     out[k].total_ms = g_prof.ms[i];
     ++k;
