@@ -48,7 +48,8 @@ enum : unsigned { F_IN_B = 1u, F_RAW = 2u };
 
 struct SplitDesc {
   unsigned long long start, size, tile_base;
-  unsigned flags, L;
+  unsigned long long aux;  // radix mode: digit multiplier M (digit = f * M >> 32)
+  unsigned flags, L;       // L: bits 0-7 fan-out exponent, bit 8 radix mode, bits 16-23 shift
 };
 
 struct Item {
@@ -247,7 +248,8 @@ struct SplSmem {
   W tree[256];  // implicit BST over srt[0..254] in BFS order (tree[1..255])
   W lo;
   unsigned cmax;
-  int shift, m, use_tree;
+  int shift, m, use_tree;  // use_tree: 0 table, 1 tree, 2 radix (equal-width digits)
+  unsigned long long mul;  // radix mode multiplier
   unsigned short lut[kLut];  // (first, end) splitter index of cell c, packed lo | hi << 8
 };
 
@@ -270,10 +272,24 @@ __host__ __device__ __forceinline__ int num_children(int L) { return 2 * ((1 << 
 // more than a few splitters (uniform-ish key codes), else the 8-level tree
 // (clustered codes, e.g. normal floats or few distinct values).
 template <typename W>
-__device__ __forceinline__ void load_splitters(const W* g_srt, int L, SplSmem<W>& S) {
+__device__ __forceinline__ void load_splitters(const W* g_srt, unsigned lraw, SplSmem<W>& S,
+                                               unsigned long long aux = 0) {
   __shared__ unsigned char first[kLut + 1];
   __shared__ int s_wide;
+  const int L = (int)(lraw & 0xFFu);
   const int m = (1 << L) - 1;
+  if (lraw & 0x100u) {  // radix mode: digit = (x - lo) >> shift, no table
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      S.lo = g_srt[0];
+      S.shift = (int)((lraw >> 16) & 0xFFu);
+      S.m = m;
+      S.mul = aux;
+      S.use_tree = 2;
+    }
+    __syncthreads();
+    return;
+  }
   for (int i = threadIdx.x; i < 255; i += blockDim.x) S.srt[i] = i < m ? g_srt[i] : key_max<W>();
   if (threadIdx.x == 0) {
     S.srt[255] = key_max<W>();
@@ -326,9 +342,17 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, int L, SplSmem<W>
 // Tree path: branch-free 8-level walk over the padded implicit BST (padding
 // with the maximum key keeps lower-bound semantics; the maximum key itself
 // lands in equality bucket 2m+1).
-template <bool TREE, typename W>
+template <int MODE, typename W>
 __device__ __forceinline__ int classify_mode(const W& x, const SplSmem<W>& S) {
-  if constexpr (TREE) {
+  if constexpr (MODE == 2) {
+    // equal-width digits over the sample range (the sample certified them
+    // balanced); keys below/above the range clamp to the first/last digit
+    const unsigned f = key_shr32(key_sub(x, S.lo), S.shift);
+    unsigned dgt = (unsigned)__umul64hi((unsigned long long)f << 32, S.mul);
+    dgt = dgt < (unsigned)S.m ? dgt : (unsigned)S.m;
+    dgt = key_lt(x, S.lo) ? 0u : dgt;
+    return 2 * (int)dgt;
+  } else if constexpr (MODE == 1) {
     int j = 1;
 #pragma unroll
     for (int l = 0; l < 8; ++l) j = 2 * j + (key_lt(S.tree[j], x) ? 1 : 0);
@@ -355,7 +379,7 @@ __device__ __forceinline__ int classify_mode(const W& x, const SplSmem<W>& S) {
 
 template <typename W>
 __device__ __forceinline__ int classify_fast(const W& x, const SplSmem<W>& S) {
-  return S.use_tree ? classify_mode<true>(x, S) : classify_mode<false>(x, S);
+  return S.use_tree == 2 ? classify_mode<2>(x, S) : (S.use_tree ? classify_mode<1>(x, S) : classify_mode<0>(x, S));
 }
 
 template <typename W>
@@ -406,6 +430,7 @@ __global__ void k_init(Params<W> P) {
     d.tile_base = 0;
     d.flags = F_RAW;
     d.L = 0;
+    d.aux = 0;
     P.split[0][0] = d;
     c->split_packed[0] = (1ull << 40) | (unsigned long long)ntiles_dev<W>(P.n);
   } else if (P.n > 1) {
@@ -427,6 +452,8 @@ template <typename W, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   W* s = reinterpret_cast<W*>(smem_raw);
+  __shared__ unsigned dcnt[256];
+  __shared__ unsigned s_maxc;
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
   const int nb = (int)(packed >> 40);
   if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrl->split_packed[P.cur ^ 1] = 0;
@@ -473,10 +500,43 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
     }
     W* g = P.splitters + (unsigned long long)p * 256;
     const int step = S / (m + 1);
-    for (int k = threadIdx.x; k < m; k += THREADS) g[k] = s[(k + 1) * step - 1];
+    // Radix certification: if equal-width digits over [sample min, max]
+    // give no digit more than ~2x its share of the sample, classify by digit
+    // (pure ALU) instead of by splitter search.
+    const W slo = s[0];
+    const W srange = key_sub(s[S - 1], slo);
+    const int bl = key_bitlen(srange);
+    const int dshift = bl > 32 ? bl - 32 : 0;  // f = top 32 bits of (x - lo)
+    const unsigned long long rf = key_shr32(srange, dshift);
+    const unsigned long long dmul = ((unsigned long long)(m + 1) << 32) / (rf + 1);
+    for (int k = threadIdx.x; k <= m; k += THREADS) dcnt[k] = 0;
+    if (threadIdx.x == 0) s_maxc = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < S; i += THREADS) {
+      const unsigned f = key_shr32(key_sub(s[i], slo), dshift);
+      unsigned dg = (unsigned)__umul64hi((unsigned long long)f << 32, dmul);
+      atomicAdd(&dcnt[dg < (unsigned)m ? dg : (unsigned)m], 1u);
+    }
+    __syncthreads();
+    unsigned used = 0;
+    for (int k = threadIdx.x; k <= m; k += THREADS) {
+      atomicMax(&s_maxc, dcnt[k]);
+      if (dcnt[k]) used = 1;
+    }
+    const unsigned nused = __syncthreads_count(used ? 1 : 0);
+    const bool radix = P.part_mode == 0 && L >= 2 && 2 * nused >= (unsigned)(m + 1) &&
+                       (unsigned)s_maxc * nused <= 2u * (unsigned)S + 4u * nused;
+    if (radix) {
+      if (threadIdx.x == 0) g[0] = slo;
+    } else {
+      for (int k = threadIdx.x; k < m; k += THREADS) g[k] = s[(k + 1) * step - 1];
+    }
     unsigned long long* cnt = P.counts + (unsigned long long)p * kChildStride;
     for (int k = threadIdx.x; k < kChildStride; k += THREADS) cnt[k] = 0;
-    if (threadIdx.x == 0) list[p].L = (unsigned)L;
+    if (threadIdx.x == 0) {
+      list[p].L = (unsigned)L | (radix ? (0x100u | ((unsigned)dshift << 16)) : 0u);
+      list[p].aux = dmul;
+    }
     __syncthreads();
   }
 }
@@ -547,8 +607,8 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
   __syncthreads();
   int p = s_p;
   SplitDesc d = list[p];
-  int L = (int)d.L;
-  load_splitters(P.splitters + (unsigned long long)p * 256, L, S);
+  int L = (int)(d.L & 0xFFu);
+  load_splitters(P.splitters + (unsigned long long)p * 256, d.L, S, d.aux);
   unsigned phase = 0;
   for (unsigned long long t = t0; t < t1; ++t) {
     const int st = (int)((t - t0) & (kStages - 1));
@@ -567,9 +627,9 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
       }
       while (p + 1 < nb && list[p + 1].tile_base <= t) ++p;
       d = list[p];
-      L = (int)d.L;
+      L = (int)(d.L & 0xFFu);
       __syncthreads();
-      load_splitters(P.splitters + (unsigned long long)p * 256, L, S);
+      load_splitters(P.splitters + (unsigned long long)p * 256, d.L, S, d.aux);
     }
     const W* src = src_of(P, d.flags);
     const int xf = (d.flags & F_RAW) ? P.xf : XF_NONE;
@@ -585,7 +645,7 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
     unsigned wide = 0;  // items whose cell holds > 2 splitters (rare)
     const Xf<W> X = make_xf<W>(xf);
     auto count_tile = [&](auto tree_tag, auto flt_tag) {
-      constexpr bool TREE = decltype(tree_tag)::value;
+      constexpr int TREE = decltype(tree_tag)::value;
       constexpr bool FLT = decltype(flt_tag)::value;
       if (cnt == TILE) {
 #pragma unroll
@@ -606,12 +666,15 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
         }
       }
     };
-    if (S.use_tree) {
-      if (X.flt) count_tile(std::true_type{}, std::true_type{});
-      else count_tile(std::true_type{}, std::false_type{});
+    if (S.use_tree == 2) {
+      if (X.flt) count_tile(std::integral_constant<int, 2>{}, std::true_type{});
+      else count_tile(std::integral_constant<int, 2>{}, std::false_type{});
+    } else if (S.use_tree) {
+      if (X.flt) count_tile(std::integral_constant<int, 1>{}, std::true_type{});
+      else count_tile(std::integral_constant<int, 1>{}, std::false_type{});
     } else {
-      if (X.flt) count_tile(std::false_type{}, std::true_type{});
-      else count_tile(std::false_type{}, std::false_type{});
+      if (X.flt) count_tile(std::integral_constant<int, 0>{}, std::true_type{});
+      else count_tile(std::integral_constant<int, 0>{}, std::false_type{});
     }
     while (wide) {
       const int i = __ffs(wide) - 1;
@@ -648,7 +711,7 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
   const int nxt = P.cur ^ 1;
   for (int p = blockIdx.x; p < nb; p += gridDim.x) {
     const SplitDesc d = list[p];
-    const int L = (int)d.L;
+    const int L = (int)(d.L & 0xFFu);
     const int nc = num_children(L);
     const int c = threadIdx.x;
     const unsigned long long cnt = c < nc ? P.counts[(unsigned long long)p * kChildStride + c] : 0;
@@ -680,6 +743,7 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
         nd.tile_base = base & kTileMask;
         nd.flags = child_flags;
         nd.L = 0;
+        nd.aux = 0;
         P.split[nxt][q] = nd;
       } else {
         P.ctrl->error = 1;
@@ -804,8 +868,8 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   __syncthreads();
   int p = s_p;
   SplitDesc d = list[p];
-  int L = (int)d.L;
-  load_splitters(P.splitters + (unsigned long long)p * 256, L, S);
+  int L = (int)(d.L & 0xFFu);
+  load_splitters(P.splitters + (unsigned long long)p * 256, d.L, S, d.aux);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   unsigned* myhist = whist + (warp % HC) * kChildStride;
@@ -822,8 +886,8 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     if (p + 1 < nb && list[p + 1].tile_base <= t) {
       while (p + 1 < nb && list[p + 1].tile_base <= t) ++p;
       d = list[p];
-      L = (int)d.L;
-      load_splitters(P.splitters + (unsigned long long)p * 256, L, S);
+      L = (int)(d.L & 0xFFu);
+      load_splitters(P.splitters + (unsigned long long)p * 256, d.L, S, d.aux);
     }
     W* dst_buf = P.part_mode ? P.out : ((d.flags & F_IN_B) ? P.a : P.b);
     const int nc = num_children(L);
@@ -845,7 +909,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     unsigned wide = 0;
     const Xf<W> X = make_xf<W>(xf);
     auto classify_tile = [&](auto tree_tag, auto flt_tag) {
-      constexpr bool TREE = decltype(tree_tag)::value;
+      constexpr int TREE = decltype(tree_tag)::value;
       constexpr bool FLT = decltype(flt_tag)::value;
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
@@ -855,12 +919,15 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
         if (bk[i] == -1) wide |= 1u << i;
       }
     };
-    if (S.use_tree) {
-      if (X.flt) classify_tile(std::true_type{}, std::true_type{});
-      else classify_tile(std::true_type{}, std::false_type{});
+    if (S.use_tree == 2) {
+      if (X.flt) classify_tile(std::integral_constant<int, 2>{}, std::true_type{});
+      else classify_tile(std::integral_constant<int, 2>{}, std::false_type{});
+    } else if (S.use_tree) {
+      if (X.flt) classify_tile(std::integral_constant<int, 1>{}, std::true_type{});
+      else classify_tile(std::integral_constant<int, 1>{}, std::false_type{});
     } else {
-      if (X.flt) classify_tile(std::false_type{}, std::true_type{});
-      else classify_tile(std::false_type{}, std::false_type{});
+      if (X.flt) classify_tile(std::integral_constant<int, 0>{}, std::true_type{});
+      else classify_tile(std::integral_constant<int, 0>{}, std::false_type{});
     }
     while (wide) {
       const int i = __ffs(wide) - 1;
