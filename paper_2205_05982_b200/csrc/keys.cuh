@@ -93,17 +93,30 @@ __host__ __device__ __forceinline__ U128 key_sub(const U128& a, const U128& b) {
   const unsigned long long lo = a.lo - b.lo;
   return U128{lo, a.hi - b.hi - (a.lo < b.lo ? 1ull : 0ull)};
 }
-// Low 32 bits of (d >> s); s may exceed the word width (returns 0).
+// (d >> s) saturated to 32 bits (0xFFFFFFFF if it does not fit); s may
+// exceed the word width (returns 0).  Saturation keeps every cell / digit
+// map monotone for keys far above a bucket's sampled range.
 __device__ __forceinline__ unsigned key_shr32(uint16_t d, int s) { return s >= 16 ? 0u : (unsigned)(d >> s); }
 __device__ __forceinline__ unsigned key_shr32(uint32_t d, int s) { return s >= 32 ? 0u : (d >> s); }
 __device__ __forceinline__ unsigned key_shr32(unsigned long long d, int s) {
-  return s >= 64 ? 0u : (unsigned)(d >> s);
+  if (s >= 64) return 0u;
+  const unsigned long long q = d >> s;
+  return q > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)q;
 }
 __device__ __forceinline__ unsigned key_shr32(const U128& d, int s) {
   if (s >= 128) return 0u;
-  if (s >= 64) return (unsigned)(d.hi >> (s - 64));
-  if (s == 0) return (unsigned)d.lo;
-  return (unsigned)((d.lo >> s) | (d.hi << (64 - s)));
+  unsigned long long qlo, qhi;
+  if (s >= 64) {
+    qlo = d.hi >> (s - 64);
+    qhi = 0;
+  } else if (s == 0) {
+    qlo = d.lo;
+    qhi = d.hi;
+  } else {
+    qlo = (d.lo >> s) | (d.hi << (64 - s));
+    qhi = d.hi >> s;
+  }
+  return (qhi != 0 || qlo > 0xFFFFFFFFull) ? 0xFFFFFFFFu : (unsigned)qlo;
 }
 // Number of significant bits.
 __device__ __forceinline__ int key_bitlen(uint16_t d) { return 32 - __clz((unsigned)d); }

@@ -179,3 +179,26 @@ def test_workspace_reuse_and_stream(cuda):
     small = torch.empty(16, dtype=torch.uint8, device="cuda")
     with pytest.raises(ValueError):
         vx.sort(torch.zeros(100_000, dtype=torch.int64, device="cuda"), workspace=small)
+
+
+def test_clustered_keys_outside_sample_range(cuda):
+    """Regression: 64/128-bit keys far above a bucket's sampled range must
+    classify monotonically (saturating cell/digit maps)."""
+    rng = np.random.default_rng(11)
+    n = 4_000_000
+    for frac in (0.5, 0.9, 0.99):
+        x = rng.integers(0, 2**64, n, dtype=np.uint64)
+        k = int(n * frac)
+        x[:k] &= np.uint64((1 << 43) - 1)
+        rng.shuffle(x)
+        for desc in (False, True):
+            check(x, "u64", desc)
+        check(x.view(np.int64), "i64", False)
+        f = rng.standard_normal(n) * 1e-3
+        f[: n // 10] *= 1e300
+        check(f, "f64", False)
+    k128 = np.empty((n // 2, 2), np.uint64)
+    k128[:, 0] = rng.integers(0, 2**64, n // 2, dtype=np.uint64)
+    k128[:, 1] = rng.integers(0, 2**64, n // 2, dtype=np.uint64)
+    k128[: n // 4, 1] &= np.uint64(0xFF)
+    check(k128, "k128", False)
