@@ -100,12 +100,24 @@ struct DevInfo {
 std::mutex g_mu;
 std::unordered_map<int, DevInfo> g_dev;
 
+// Keep stream-ordered allocations (workspace, host-path key buffers) cached
+// in the device's default pool instead of returning them at every sync.
+void ensure_pool(int dev, DevInfo& di) {
+  if (di.sms != 0) return;
+  cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
 int grid_for(const void* fn, int threads, size_t smem) {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_mu);
   DevInfo& di = g_dev[dev];
-  if (di.sms == 0) cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
+  ensure_pool(dev, di);
   auto it = di.occ.find(fn);
   int occ;
   if (it == di.occ.end()) {
@@ -489,6 +501,12 @@ vxs_status vxs_sort_host(void* h_keys, size_t n, vxs_key_type type, vxs_order or
   if (n <= 1) return VXS_OK;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(VXS_NO_DEVICE, "vxsort_b200: no CUDA device");
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_mu);
+    ensure_pool(dev, g_dev[dev]);
+  }
   cudaStream_t st;
   VXS_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream create");
   void* d = nullptr;
