@@ -34,8 +34,9 @@
 
 namespace vxs {
 
-constexpr int kMaxL = 8;            // up to 256-way split per level
-constexpr int kChildStride = 512;   // child slots per split bucket (2*255+1 used)
+constexpr int kMaxL = 8;            // up to 256-way splitter-based split per level
+constexpr int kMaxRadixL = 8;       // radix-certified split fan-out cap (9 measured slower: cursor contention)
+constexpr int kChildStride = 512;   // child slots per split bucket (2*(2^L-1)+2 used)
 constexpr int kNumSortClasses = 5;  // base-case size classes
 constexpr int kListCopySmall = kNumSortClasses;
 constexpr int kListCopyBig = kNumSortClasses + 1;
@@ -165,8 +166,11 @@ struct Params {
   Ctrl* ctrl;
   SplitDesc* split[2];
   W* splitters;                 // [cap_split][256]
-  unsigned long long* counts;   // [cap_split][kChildStride]
-  unsigned long long* cursors;  // [cap_split][kChildStride]
+  unsigned long long* counts;   // [cap_split][kChildStride] per-child totals (k_plan)
+  unsigned long long* seg;      // [cap_split + grid][kChildStride] per-(bucket p, CTA b) child
+                                //   counts (k_hist) -> absolute offsets (k_plan), slot p + b
+  unsigned long long* childbase;  // [cap_split][kChildStride] absolute start of each child
+  int grid;                     // CTAs of k_hist and k_scatter (identical tile ranges)
   Item* items[kNumLists];
   unsigned long long cap_split, cap_items;
   W* out;                       // part_mode output
@@ -452,7 +456,7 @@ template <typename W, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   W* s = reinterpret_cast<W*>(smem_raw);
-  __shared__ unsigned dcnt[256];
+  __shared__ unsigned dcnt[1 << kMaxRadixL];
   __shared__ unsigned s_maxc;
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
   const int nb = (int)(packed >> 40);
@@ -502,39 +506,49 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
     const int step = S / (m + 1);
     // Radix certification: if equal-width digits over [sample min, max]
     // give no digit more than ~2x its share of the sample, classify by digit
-    // (pure ALU) instead of by splitter search.
+    // (pure ALU) instead of by splitter search.  Radix buckets may split up
+    // to 2^kMaxRadixL ways (no splitter table is needed).
     const W slo = s[0];
     const W srange = key_sub(s[S - 1], slo);
     const int bl = key_bitlen(srange);
     const int dshift = bl > 32 ? bl - 32 : 0;  // f = top 32 bits of (x - lo)
     const unsigned long long rf = key_shr32(srange, dshift);
-    const unsigned long long dmul = ((unsigned long long)(m + 1) << 32) / (rf + 1);
-    for (int k = threadIdx.x; k <= m; k += THREADS) dcnt[k] = 0;
-    if (threadIdx.x == 0) s_maxc = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < S; i += THREADS) {
-      const unsigned f = key_shr32(key_sub(s[i], slo), dshift);
-      unsigned dg = (unsigned)__umul64hi((unsigned long long)f << 32, dmul);
-      atomicAdd(&dcnt[dg < (unsigned)m ? dg : (unsigned)m], 1u);
+    auto certify = [&](int Lr, unsigned long long& mul) -> bool {
+      const int mr = (1 << Lr) - 1;
+      mul = ((unsigned long long)(mr + 1) << 32) / (rf + 1);
+      for (int k = threadIdx.x; k <= mr; k += THREADS) dcnt[k] = 0;
+      if (threadIdx.x == 0) s_maxc = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < S; i += THREADS) {
+        const unsigned f = key_shr32(key_sub(s[i], slo), dshift);
+        const unsigned dg = (unsigned)__umul64hi((unsigned long long)f << 32, mul);
+        atomicAdd(&dcnt[dg < (unsigned)mr ? dg : (unsigned)mr], 1u);
+      }
+      __syncthreads();
+      unsigned used = 0;
+      for (int k = threadIdx.x; k <= mr; k += THREADS) {
+        atomicMax(&s_maxc, dcnt[k]);
+        if (dcnt[k]) used = 1;
+      }
+      const unsigned nused = __syncthreads_count(used ? 1 : 0);
+      return P.part_mode == 0 && Lr >= 2 && 2 * nused >= (unsigned)(mr + 1) &&
+             (unsigned)s_maxc * nused <= 2u * (unsigned)S + 4u * nused;
+    };
+    unsigned long long dmul = 0;
+    int Lf = L;
+    bool radix = false;
+    if (L == kMaxL && (d.size >> kMaxL) > (unsigned long long)(Cfg<W>::kCap / 4)) {
+      radix = certify(kMaxRadixL, dmul);
+      if (radix) Lf = kMaxRadixL;
     }
-    __syncthreads();
-    unsigned used = 0;
-    for (int k = threadIdx.x; k <= m; k += THREADS) {
-      atomicMax(&s_maxc, dcnt[k]);
-      if (dcnt[k]) used = 1;
-    }
-    const unsigned nused = __syncthreads_count(used ? 1 : 0);
-    const bool radix = P.part_mode == 0 && L >= 2 && 2 * nused >= (unsigned)(m + 1) &&
-                       (unsigned)s_maxc * nused <= 2u * (unsigned)S + 4u * nused;
+    if (!radix) radix = certify(L, dmul);
     if (radix) {
       if (threadIdx.x == 0) g[0] = slo;
     } else {
       for (int k = threadIdx.x; k < m; k += THREADS) g[k] = s[(k + 1) * step - 1];
     }
-    unsigned long long* cnt = P.counts + (unsigned long long)p * kChildStride;
-    for (int k = threadIdx.x; k < kChildStride; k += THREADS) cnt[k] = 0;
     if (threadIdx.x == 0) {
-      list[p].L = (unsigned)L | (radix ? (0x100u | ((unsigned)dshift << 16)) : 0u);
+      list[p].L = (unsigned)Lf | (radix ? (0x100u | ((unsigned)dshift << 16)) : 0u);
       list[p].aux = dmul;
     }
     __syncthreads();
@@ -621,8 +635,9 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
     if (p + 1 < nb && list[p + 1].tile_base <= t) {
       // flush and move to the next bucket
       const int nc = num_children(L);
+      unsigned long long* sg = P.seg + (unsigned long long)(p + blockIdx.x) * kChildStride;
       for (int c = threadIdx.x; c < nc; c += THREADS) {
-        if (hist[c]) atomicAdd(P.counts + (unsigned long long)p * kChildStride + c, (unsigned long long)hist[c]);
+        sg[c] = hist[c];
         hist[c] = 0;
       }
       while (p + 1 < nb && list[p + 1].tile_base <= t) ++p;
@@ -684,8 +699,50 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
     __syncthreads();  // stage st fully consumed before it is refilled
   }
   const int nc = num_children(L);
-  for (int c = threadIdx.x; c < nc; c += THREADS) {
-    if (hist[c]) atomicAdd(P.counts + (unsigned long long)p * kChildStride + c, (unsigned long long)hist[c]);
+  unsigned long long* sg = P.seg + (unsigned long long)(p + blockIdx.x) * kChildStride;
+  for (int c = threadIdx.x; c < nc; c += THREADS) sg[c] = hist[c];
+}
+
+// Column scan of the per-(bucket p, CTA b) child counts written by k_hist:
+// slot (p + b) becomes the offset of CTA b's keys inside child c, and the
+// per-child totals go to counts[p][c].  Work item = (bucket, 32 children);
+// one warp per item, 16 independent loads in flight per lane.
+template <typename W>
+__global__ void __launch_bounds__(128) k_segscan(Params<W> P) {
+  const unsigned long long packed = P.ctrl->split_packed[P.cur];
+  const int nb = (int)(packed >> 40);
+  const unsigned long long T = packed & kTileMask;
+  if (nb == 0) return;
+  const unsigned long long tpc = (T + P.grid - 1) / P.grid;
+  const SplitDesc* list = P.split[P.cur];
+  constexpr int kChunks = kChildStride / 32;
+  const int lane = threadIdx.x & 31;
+  const long long nwork = (long long)nb * kChunks;
+  for (long long w = (long long)blockIdx.x * 4 + (threadIdx.x >> 5); w < nwork; w += (long long)gridDim.x * 4) {
+    const int p = (int)(w / kChunks);
+    const int c = (int)(w % kChunks) * 32 + lane;
+    const SplitDesc d = list[p];
+    const int nc = num_children((int)(d.L & 0xFFu));
+    if ((int)(w % kChunks) * 32 >= nc) continue;
+    const unsigned long long nt = (unsigned long long)ntiles_dev<W>(d.size);
+    const int b_first = (int)(d.tile_base / tpc);
+    const int b_last = (int)((d.tile_base + nt - 1) / tpc);
+    unsigned long long cnt = 0;
+    if (c < nc) {
+      constexpr int B = 16;
+      for (int b0 = b_first; b0 <= b_last; b0 += B) {
+        unsigned long long v[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j)
+          v[j] = b0 + j <= b_last ? P.seg[(unsigned long long)(p + b0 + j) * kChildStride + c] : 0ull;
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+          if (b0 + j <= b_last) P.seg[(unsigned long long)(p + b0 + j) * kChildStride + c] = cnt;
+          cnt += v[j];
+        }
+      }
+      P.counts[(unsigned long long)p * kChildStride + c] = cnt;
+    }
   }
 }
 
@@ -714,10 +771,11 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
     const int L = (int)(d.L & 0xFFu);
     const int nc = num_children(L);
     const int c = threadIdx.x;
-    const unsigned long long cnt = c < nc ? P.counts[(unsigned long long)p * kChildStride + c] : 0;
+    // per-child totals were reduced over the touching CTAs by k_segscan
+    const unsigned long long cnt = c < nc ? P.counts[(unsigned long long)p * kChildStride + c] : 0ull;
     unsigned long long total;
     const unsigned long long off = block_exclusive_scan<THREADS>(cnt, &total, scan_scratch);
-    if (c < nc) P.cursors[(unsigned long long)p * kChildStride + c] = d.start + off;
+    if (c < nc) P.childbase[(unsigned long long)p * kChildStride + c] = d.start + off;
     s_cnt[c] = cnt;
     s_off[c] = off;
     const unsigned child_flags = (d.flags & F_IN_B) ? 0u : F_IN_B;  // raw cleared
@@ -844,6 +902,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   unsigned* whist = reinterpret_cast<unsigned*>(stage_b + TILE);  // [HC][kChildStride]
   __shared__ SplSmem<W> S;
   __shared__ long long gdelta[kChildStride];  // global index of staged slot 0 of child c
+  __shared__ unsigned long long gcur[kChildStride];  // this CTA's next global slot per child
   __shared__ unsigned scan_scratch[32];
   __shared__ __align__(8) unsigned long long bars[kStages];
   __shared__ int s_p;
@@ -870,6 +929,13 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   SplitDesc d = list[p];
   int L = (int)(d.L & 0xFFu);
   load_splitters(P.splitters + (unsigned long long)p * 256, d.L, S, d.aux);
+  auto load_cursors = [&]() {
+    const unsigned long long* sg = P.seg + (unsigned long long)(p + blockIdx.x) * kChildStride;
+    const unsigned long long* cb = P.childbase + (unsigned long long)p * kChildStride;
+    const int ncl = num_children(L);
+    for (int c = threadIdx.x; c < ncl; c += THREADS) gcur[c] = cb[c] + sg[c];
+  };
+  load_cursors();
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   unsigned* myhist = whist + (warp % HC) * kChildStride;
@@ -888,6 +954,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       d = list[p];
       L = (int)(d.L & 0xFFu);
       load_splitters(P.splitters + (unsigned long long)p * 256, d.L, S, d.aux);
+      load_cursors();
     }
     W* dst_buf = P.part_mode ? P.out : ((d.flags & F_IN_B) ? P.a : P.b);
     const int nc = num_children(L);
@@ -981,9 +1048,11 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
           whist[w * kChildStride + c] = run;
           run += v;
         }
-        gres[j] = (tot[j] && c < nc)
-                      ? atomicAdd(P.cursors + (unsigned long long)p * kChildStride + c, (unsigned long long)tot[j])
-                      : 0ull;
+        gres[j] = 0;
+        if (tot[j] && c < nc) {  // private cursor: no global atomics
+          gres[j] = gcur[c];
+          gcur[c] += tot[j];
+        }
         exc[j] = ex;
         ex += tot[j];
       }

@@ -43,10 +43,10 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // ---- optional per-kernel event timing (measurement tools only) -----------
 enum KernelId : int {
-  K_INIT = 0, K_SAMPLE, K_HIST, K_PLAN, K_SCATTER, K_FINAL0, K_FINAL1, K_FINAL2, K_FINAL3, K_FINAL4,
+  K_INIT = 0, K_SAMPLE, K_HIST, K_SEGSCAN, K_PLAN, K_SCATTER, K_FINAL0, K_FINAL1, K_FINAL2, K_FINAL3, K_FINAL4,
   K_FALLBACK, K_COPY, K_PART, K_MISC, K_COUNT
 };
-const char* kKernelNames[K_COUNT] = {"k_init", "k_sample", "k_hist", "k_plan", "k_scatter", "k_final_c0",
+const char* kKernelNames[K_COUNT] = {"k_init", "k_sample", "k_hist", "k_segscan", "k_plan", "k_scatter", "k_final_c0",
                                      "k_final_c1", "k_final_c2", "k_final_c3", "k_final_c4",
                                      "k_final_fallback", "k_copy", "k_part", "k_misc"};
 struct Prof {
@@ -133,8 +133,24 @@ int grid_for(const void* fn, int threads, size_t smem) {
 }
 
 // ---- workspace layout ------------------------------------------------------
+constexpr int kMaxGrid = 4096;  // upper bound on the streaming kernels' grid
+
+template <typename W>
+constexpr size_t hist_smem();
+template <typename W>
+constexpr size_t scatter_smem();
+
+// k_hist and k_scatter run with the SAME grid so CTA b owns the same tile
+// range in both (the per-(bucket, CTA) offset table relies on it).
+template <typename W>
+int stream_grid() {
+  const int gh = grid_for((const void*)k_hist<W>, Cfg<W>::kHistThreads, hist_smem<W>());
+  const int gs = grid_for((const void*)k_scatter<W>, Cfg<W>::kScatThreads, scatter_smem<W>());
+  int g = gh < gs ? gh : gs;
+  return g < kMaxGrid ? g : kMaxGrid;
+}
 struct Layout {
-  size_t tmp, split0, split1, splitters, counts, cursors, items[kNumLists], ctrl, total;
+  size_t tmp, split0, split1, splitters, counts, childbase, seg, items[kNumLists], ctrl, total;
   unsigned long long cap_split, cap_items;
 };
 
@@ -155,7 +171,8 @@ Layout layout_for(size_t n) {
   L.split1 = take(L.cap_split * sizeof(SplitDesc));
   L.splitters = take(L.cap_split * 256 * sizeof(W));
   L.counts = take(L.cap_split * kChildStride * sizeof(unsigned long long));
-  L.cursors = take(L.cap_split * kChildStride * sizeof(unsigned long long));
+  L.childbase = take(L.cap_split * kChildStride * sizeof(unsigned long long));
+  L.seg = take((L.cap_split + kMaxGrid) * kChildStride * sizeof(unsigned long long));
   for (int i = 0; i < kNumLists; ++i) L.items[i] = take(L.cap_items * sizeof(Item));
   L.ctrl = take(sizeof(Ctrl));
   L.total = off;
@@ -178,7 +195,9 @@ Params<W> make_params(W* keys, size_t n, int xf, uint64_t seed, unsigned char* w
   P.split[1] = reinterpret_cast<SplitDesc*>(ws + L.split1);
   P.splitters = reinterpret_cast<W*>(ws + L.splitters);
   P.counts = reinterpret_cast<unsigned long long*>(ws + L.counts);
-  P.cursors = reinterpret_cast<unsigned long long*>(ws + L.cursors);
+  P.seg = reinterpret_cast<unsigned long long*>(ws + L.seg);
+  P.childbase = reinterpret_cast<unsigned long long*>(ws + L.childbase);
+  P.grid = stream_grid<W>();
   for (int i = 0; i < kNumLists; ++i) P.items[i] = reinterpret_cast<Item*>(ws + L.items[i]);
   P.cap_split = L.cap_split;
   P.cap_items = L.cap_items;
@@ -223,8 +242,13 @@ vxs_status launch_level(Params<W>& P, cudaStream_t st, int& launches) {
   {
     ProfScope ps(K_HIST + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
     auto fn = k_hist<W>;
-    const int g = grid_for((const void*)fn, Cfg<W>::kHistThreads, hist_smem<W>());
-    fn<<<g, Cfg<W>::kHistThreads, hist_smem<W>(), st>>>(P);
+    fn<<<P.grid, Cfg<W>::kHistThreads, hist_smem<W>(), st>>>(P);
+  }
+  {
+    ProfScope ps(K_SEGSCAN + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
+    auto fn = k_segscan<W>;
+    const int g = grid_for((const void*)fn, 128, 0);
+    fn<<<g, 128, 0, st>>>(P);
   }
   {
     ProfScope ps(K_PLAN + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
@@ -235,10 +259,9 @@ vxs_status launch_level(Params<W>& P, cudaStream_t st, int& launches) {
   {
     ProfScope ps(K_SCATTER + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
     auto fn = k_scatter<W>;
-    const int g = grid_for((const void*)fn, Cfg<W>::kScatThreads, scatter_smem<W>());
-    fn<<<g, Cfg<W>::kScatThreads, scatter_smem<W>(), st>>>(P);
+    fn<<<P.grid, Cfg<W>::kScatThreads, scatter_smem<W>(), st>>>(P);
   }
-  launches += 4;
+  launches += 5;
   VXS_CK(cudaGetLastError(), "level launch");
   return VXS_OK;
 }
@@ -592,14 +615,13 @@ vxs_status vxs_partition(const void* d_keys, size_t n, vxs_key_type type, vxs_or
     k_part_setup<W><<<1, 256, 0, st>>>(P, static_cast<const W*>(d_splitters), nspl, L);
     {
       auto fn = k_hist<W>;
-      const int g = grid_for((const void*)fn, Cfg<W>::kHistThreads, hist_smem<W>());
-      fn<<<g, Cfg<W>::kHistThreads, hist_smem<W>(), st>>>(P);
+      fn<<<P.grid, Cfg<W>::kHistThreads, hist_smem<W>(), st>>>(P);
     }
+    k_segscan<W><<<16, 128, 0, st>>>(P);
     k_plan<W><<<1, kChildStride, 0, st>>>(P);
     {
       auto fn = k_scatter<W>;
-      const int g = grid_for((const void*)fn, Cfg<W>::kScatThreads, scatter_smem<W>());
-      fn<<<g, Cfg<W>::kScatThreads, scatter_smem<W>(), st>>>(P);
+      fn<<<P.grid, Cfg<W>::kScatThreads, scatter_smem<W>(), st>>>(P);
     }
     k_part_counts<W><<<1, 256, 0, st>>>(P, nseg, reinterpret_cast<unsigned long long*>(d_seg_counts));
     VXS_CK(cudaGetLastError(), "partition");
