@@ -141,6 +141,10 @@ struct SortClass<4> {
   static constexpr bool kWarpNet = false;
 };
 
+// Radix-mode buckets aim for final items of about this many keys (just
+// under the 2048-key base-case class).
+constexpr double kFinalTarget = 1900.0;
+
 // Adjacent small children are grouped into one base-case item until the
 // group holds at least this many keys (never more than Cap).
 constexpr unsigned long long kGroupTarget = 1024;
@@ -513,9 +517,9 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
     const int bl = key_bitlen(srange);
     const int dshift = bl > 32 ? bl - 32 : 0;  // f = top 32 bits of (x - lo)
     const unsigned long long rf = key_shr32(srange, dshift);
-    auto certify = [&](int Lr, unsigned long long& mul) -> bool {
-      const int mr = (1 << Lr) - 1;
-      mul = ((unsigned long long)(mr + 1) << 32) / (rf + 1);
+    auto certify = [&](int D, unsigned long long& mul) -> bool {
+      const int mr = D - 1;
+      mul = ((unsigned long long)D << 32) / (rf + 1);
       for (int k = threadIdx.x; k <= mr; k += THREADS) dcnt[k] = 0;
       if (threadIdx.x == 0) s_maxc = 0;
       __syncthreads();
@@ -531,17 +535,30 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
         if (dcnt[k]) used = 1;
       }
       const unsigned nused = __syncthreads_count(used ? 1 : 0);
-      return P.part_mode == 0 && Lr >= 2 && 2 * nused >= (unsigned)(mr + 1) &&
+      return P.part_mode == 0 && D >= 4 && 2 * nused >= (unsigned)D &&
              (unsigned)s_maxc * nused <= 2u * (unsigned)S + 4u * nused;
     };
+    // Radix fan-out balanced over the levels still needed so the final
+    // items land just under the base case's 2048-key class.
+    int Dr;
+    {
+      const double ratio = (double)d.size / (double)kFinalTarget;
+      int lv = 1;
+      double Dd = ratio;
+      while (Dd > 256.0) {
+        ++lv;
+        Dd = pow(ratio, 1.0 / lv);
+      }
+      Dr = (int)ceil(Dd);
+      Dr = Dr < 4 ? 4 : (Dr > 256 ? 256 : Dr);
+    }
     unsigned long long dmul = 0;
     int Lf = L;
-    bool radix = false;
-    if (L == kMaxL && (d.size >> kMaxL) > (unsigned long long)(Cfg<W>::kCap / 4)) {
-      radix = certify(kMaxRadixL, dmul);
-      if (radix) Lf = kMaxRadixL;
+    bool radix = certify(Dr, dmul);
+    if (radix) {
+      Lf = 2;
+      while ((1 << Lf) < Dr) ++Lf;
     }
-    if (!radix) radix = certify(L, dmul);
     if (radix) {
       if (threadIdx.x == 0) g[0] = slo;
     } else {
