@@ -535,8 +535,10 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
         if (dcnt[k]) used = 1;
       }
       const unsigned nused = __syncthreads_count(used ? 1 : 0);
+      // every digit within ~2x of the mean over ALL D digits: children stay
+      // <= ~2x the target size, so certification never adds a level
       return P.part_mode == 0 && D >= 4 && 2 * nused >= (unsigned)D &&
-             (unsigned)s_maxc * nused <= 2u * (unsigned)S + 4u * nused;
+             (unsigned)s_maxc * (unsigned)D <= 2u * (unsigned)S + 4u * (unsigned)D;
     };
     // Radix fan-out balanced over the levels still needed so the final
     // items land just under the base case's 2048-key class.
@@ -545,9 +547,13 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
       const double ratio = (double)d.size / (double)kFinalTarget;
       int lv = 1;
       double Dd = ratio;
-      while (Dd > 256.0) {
-        ++lv;
-        Dd = pow(ratio, 1.0 / lv);
+      // one level while 256-way children still fit the base case (small
+      // inputs: an extra level costs more than a fuller base case saves)
+      if (Dd * kFinalTarget > 256.0 * Cfg<W>::kCap) {
+        while (Dd > 256.0) {
+          ++lv;
+          Dd = pow(ratio, 1.0 / lv);
+        }
       }
       Dr = (int)ceil(Dd);
       Dr = Dr < 4 ? 4 : (Dr > 256 ? 256 : Dr);
