@@ -64,15 +64,11 @@ void run(const char* name, int item) {
 }
 
 int main() {
-  run<unsigned, 256, 16, false>("u32 256x16 merge", 4096);
-  run<unsigned, 128, 16, false>("u32 128x16 merge", 2048);
-  run<unsigned, 64, 16, false>("u32 64x16 merge", 1024);
-  run<unsigned, 128, 8, false>("u32 128x8 merge", 1024);
-  run<unsigned, 64, 16, true>("u32 64x16 warpnet", 1024);
   run<unsigned, 128, 16, true>("u32 128x16 warpnet", 2048);
-  run<unsigned, 256, 16, true>("u32 256x16 warpnet", 4096);
-  run<unsigned long long, 256, 16, false>("u64 256x16 merge", 4096);
-  run<unsigned long long, 128, 16, false>("u64 128x16 merge", 2048);
-  run<unsigned long long, 128, 16, true>("u64 128x16 warpnet", 2048);
+  run<unsigned, 32, 64, true>("u32 32x64 warpnet", 2048);
+  run<unsigned, 32, 32, true>("u32 32x32 warpnet", 1024);
+  run<unsigned, 64, 16, true>("u32 64x16 warpnet", 1024);
+  run<unsigned, 128, 16, true>("u32 128x16 warpnet", 1900);
+  run<unsigned, 32, 64, true>("u32 32x64 warpnet", 1900);
   return 0;
 }
