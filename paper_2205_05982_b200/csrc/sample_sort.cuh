@@ -385,6 +385,24 @@ __device__ __forceinline__ int classify_mode(const W& x, const SplSmem<W>& S) {
   }
 }
 
+// Radix-mode classifier parameters hoisted into registers (the write-out
+// loop of k_scatter recomputes child ids instead of staging them in smem).
+template <typename W>
+struct RadixReg {
+  W lo;
+  int shift;
+  unsigned m;
+  unsigned long long mul;
+  __device__ __forceinline__ explicit RadixReg(const SplSmem<W>& S) : lo(S.lo), shift(S.shift), m((unsigned)S.m), mul(S.mul) {}
+  __device__ __forceinline__ int child(const W& x) const {
+    const unsigned f = key_shr32(key_sub(x, lo), shift);
+    unsigned dgt = (unsigned)__umul64hi((unsigned long long)f << 32, mul);
+    dgt = dgt < m ? dgt : m;
+    dgt = key_lt(x, lo) ? 0u : dgt;
+    return 2 * (int)dgt;
+  }
+};
+
 template <typename W>
 __device__ __forceinline__ int classify_fast(const W& x, const SplSmem<W>& S) {
   return S.use_tree == 2 ? classify_mode<2>(x, S) : (S.use_tree ? classify_mode<1>(x, S) : classify_mode<0>(x, S));
@@ -998,6 +1016,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     int bk[ITEMS];
     unsigned wide = 0;
     const Xf<W> X = make_xf<W>(xf);
+    const bool radix = sizeof(W) <= 4 && S.use_tree == 2;  // recompute ids (cheap for <= 32-bit words)
     auto classify_tile = [&](auto tree_tag, auto flt_tag) {
       constexpr int TREE = decltype(tree_tag)::value;
       constexpr bool FLT = decltype(flt_tag)::value;
@@ -1081,13 +1100,20 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       }
       __syncthreads();
       W* staged = reinterpret_cast<W*>(stage);
+      if (radix) {  // child ids are recomputed from the keys at write-out
 #pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        if (bk[i] >= 0) {
-          const int c = bk[i] >> 16;
-          const unsigned pos = myhist[c] + (unsigned)(bk[i] & 0xFFFF);
-          staged[pos] = k[i];
-          stage_b[pos] = (unsigned short)c;
+        for (int i = 0; i < ITEMS; ++i) {
+          if (bk[i] >= 0) staged[myhist[bk[i] >> 16] + (unsigned)(bk[i] & 0xFFFF)] = k[i];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          if (bk[i] >= 0) {
+            const int c = bk[i] >> 16;
+            const unsigned pos = myhist[c] + (unsigned)(bk[i] & 0xFFFF);
+            staged[pos] = k[i];
+            stage_b[pos] = (unsigned short)c;
+          }
         }
       }
 #pragma unroll
@@ -1098,7 +1124,20 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     }
     W* staged = reinterpret_cast<W*>(stage);
     __syncthreads();
-    if (out_xf == XF_NONE) {
+    if (radix) {
+      const RadixReg<W> R(S);
+      if (out_xf == XF_NONE) {
+        for (int j = threadIdx.x; j < cnt; j += THREADS) {
+          const W v = staged[j];
+          dst_buf[gdelta[R.child(v)] + j] = v;
+        }
+      } else {
+        for (int j = threadIdx.x; j < cnt; j += THREADS) {
+          const W v = staged[j];
+          dst_buf[gdelta[R.child(v)] + j] = dec<W>(v, out_xf);
+        }
+      }
+    } else if (out_xf == XF_NONE) {
       for (int j = threadIdx.x; j < cnt; j += THREADS) dst_buf[gdelta[stage_b[j]] + j] = staged[j];
     } else {  // vxs_partition: decode into the caller's encoding
       for (int j = threadIdx.x; j < cnt; j += THREADS) dst_buf[gdelta[stage_b[j]] + j] = dec<W>(staged[j], out_xf);
