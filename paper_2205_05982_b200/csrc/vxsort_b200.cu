@@ -9,13 +9,18 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
 #include "../../include/vxsort_b200.h"
+#include "host_pipe.cuh"
 #include "sample_sort.cuh"
 
 namespace vxs {
@@ -280,6 +285,51 @@ void launch_final(Params<W>& P, unsigned long long count, cudaStream_t st) {
   fn<<<g, T, smem, st>>>(P);
 }
 
+// Control-block readback through mapped pinned memory written by a 1-warp
+// kernel: no copy engine involved, so the per-call sync never queues behind
+// a large D2H transfer on another stream (host pipeline, user copies).
+__global__ void k_ctrl_out(const Ctrl* c, Ctrl* out) {
+  const unsigned* s = reinterpret_cast<const unsigned*>(c);
+  volatile unsigned* d = reinterpret_cast<volatile unsigned*>(out);
+  for (int i = threadIdx.x; i < (int)(sizeof(Ctrl) / 4); i += 32) d[i] = s[i];
+  __threadfence_system();
+}
+
+struct CtrlMirror {
+  std::unordered_map<int, Ctrl*> buf;
+  ~CtrlMirror() {
+    for (auto& kv : buf) cudaFreeHost(kv.second);
+  }
+};
+
+// Per (thread, device) mapped mirror; run_sort has at most one outstanding
+// readback per thread (it synchronises before returning).
+Ctrl* ctrl_mirror() {
+  thread_local CtrlMirror m;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto it = m.buf.find(dev);
+  if (it != m.buf.end()) return it->second;
+  Ctrl* p = nullptr;
+  if (cudaHostAlloc(reinterpret_cast<void**>(&p), sizeof(Ctrl), cudaHostAllocMapped) != cudaSuccess) return nullptr;
+  m.buf[dev] = p;
+  return p;
+}
+
+vxs_status read_ctrl(const Ctrl* d_ctrl, Ctrl& h, cudaStream_t st) {
+  Ctrl* m = ctrl_mirror();
+  if (m == nullptr) {
+    VXS_CK(cudaMemcpyAsync(&h, d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st), "ctrl readback");
+    VXS_CK(cudaStreamSynchronize(st), "ctrl sync");
+    return VXS_OK;
+  }
+  k_ctrl_out<<<1, 32, 0, st>>>(d_ctrl, m);
+  VXS_CK(cudaGetLastError(), "ctrl readback");
+  VXS_CK(cudaStreamSynchronize(st), "ctrl sync");
+  std::memcpy(&h, const_cast<const Ctrl*>(m), sizeof(Ctrl));
+  return VXS_OK;
+}
+
 template <typename W>
 vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t ws_bytes, cudaStream_t st,
                     vxs_stats* stats) {
@@ -317,8 +367,11 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
         P.cur ^= 1;
         ++levels;
       }
-      VXS_CK(cudaMemcpyAsync(&h, P.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st), "ctrl readback");
-      VXS_CK(cudaStreamSynchronize(st), "level sync");
+      {
+        const vxs_status rs = read_ctrl(P.ctrl, h, st);
+        if (rs != VXS_OK) return rs;
+        ++launches;
+      }
       if (h.error) {  // (final-phase overflow is checked by the error flag below)
         if (owned) cudaFreeAsync(owned, st);
         return fail(VXS_INTERNAL, "vxsort_b200: device scheduler list overflow");
@@ -332,8 +385,9 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
       }
     }
   } else {
-    VXS_CK(cudaMemcpyAsync(&h, P.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st), "ctrl readback");
-    VXS_CK(cudaStreamSynchronize(st), "ctrl sync");
+    const vxs_status rs = read_ctrl(P.ctrl, h, st);
+    if (rs != VXS_OK) return rs;
+    ++launches;
   }
   if (h.item_count[0]) { launch_final<W, 0>(P, h.item_count[0], st); ++launches; }
   if (h.item_count[1]) { launch_final<W, 1>(P, h.item_count[1], st); ++launches; }
@@ -422,6 +476,467 @@ __global__ void k_xform(W* keys, unsigned long long n, int xf, int inverse) {
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x)
     keys[i] = inverse ? dec<W>(keys[i], xf) : enc<W>(keys[i], xf);
+}
+
+// ---- host-pointer pipeline (kernels in host_pipe.cuh) --------
+
+// Host-side "first k stages are ready" counter shared with a copy thread.
+struct Ready {
+  std::mutex mu;
+  std::condition_variable cv;
+  int k = 0;
+  void post(int v) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      k = v;
+    }
+    cv.notify_all();
+  }
+  void wait(int v) {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return k >= v; });
+  }
+};
+
+// Fixed pool of host threads for pageable <-> pinned staging copies (one
+// memcpy thread measured ~14 GB/s on the GPU box's host, 8 threads ~60 GB/s,
+// i.e. faster than PCIe).
+class CopyPool {
+ public:
+  explicit CopyPool(int nthreads) : n_(nthreads) {
+    for (int i = 0; i < n_; ++i) th_.emplace_back([this, i] { loop(i); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  // Parallel memcpy; returns when every part is copied.
+  void copy(void* dst, const void* src, size_t bytes) {
+    if (bytes < (size_t(1) << 20)) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    std::unique_lock<std::mutex> lk(mu_);
+    dst_ = static_cast<unsigned char*>(dst);
+    src_ = static_cast<const unsigned char*>(src);
+    bytes_ = bytes;
+    pending_ = n_;
+    ++gen_;
+    cv_.notify_all();
+    done_.wait(lk, [&] { return pending_ == 0; });
+  }
+
+ private:
+  void loop(int i) {
+    unsigned long long seen = 0;
+    for (;;) {
+      unsigned char* d;
+      const unsigned char* s;
+      size_t b;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        d = dst_;
+        s = src_;
+        b = bytes_;
+      }
+      const size_t per = ((b + n_ - 1) / n_ + 63) & ~size_t(63);  // n_ * per >= b
+      const size_t lo = std::min(b, per * i), hi = std::min(b, lo + per);
+      if (hi > lo) std::memcpy(d + lo, s + lo, hi - lo);
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (--pending_ == 0) done_.notify_all();
+      }
+    }
+  }
+  int n_;
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  unsigned char* dst_ = nullptr;
+  const unsigned char* src_ = nullptr;
+  size_t bytes_ = 0;
+  int pending_ = 0;
+  unsigned long long gen_ = 0;
+  bool stop_ = false;
+};
+
+constexpr int kMergeStreams = 4;
+constexpr int kStageSlots = 4;                        // per direction
+constexpr size_t kStageBytes = size_t(8) << 20;       // per slot
+
+// Per-device pipeline context: streams, events and the pinned staging ring,
+// created once and reused (one host-pointer sort at a time per device).
+struct PipeCtx {
+  int dev = 0;
+  cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr, s_mrg[kMergeStreams] = {};
+  cudaEvent_t ev_in[kPipeMaxChunks], ev_sl[kPipeMaxSlices], ev_alloc, ev_done, ev_mrg[kMergeStreams];
+  unsigned char* stage = nullptr;  // 2 * kStageSlots * kStageBytes pinned
+  cudaEvent_t ev_stage[2 * kStageSlots];
+  std::unique_ptr<CopyPool> pool;
+  std::mutex busy;
+  bool ok = false;
+  explicit PipeCtx(int d) : dev(d) {
+    bool good = cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&s_cmp, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking) == cudaSuccess;
+    for (auto& s : s_mrg) good = good && cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess;
+    for (auto& e : ev_in) good = good && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+    for (auto& e : ev_sl) good = good && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+    for (auto& e : ev_mrg) good = good && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+    for (auto& e : ev_stage) good = good && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+    good = good && cudaEventCreateWithFlags(&ev_alloc, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) == cudaSuccess;
+    ok = good;
+  }
+  // Pinned staging ring + copy threads, only when a pageable source shows up.
+  bool ensure_staging() {
+    if (stage) return true;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&stage), 2 * kStageSlots * kStageBytes, cudaHostAllocDefault) !=
+        cudaSuccess) {
+      stage = nullptr;
+      cudaGetLastError();
+      return false;
+    }
+    const unsigned hc = std::thread::hardware_concurrency();
+    pool = std::make_unique<CopyPool>((int)std::max(1u, std::min(8u, hc ? hc / 2 : 4u)));
+    return true;
+  }
+  unsigned char* slot(int i) { return stage + (size_t)i * kStageBytes; }
+};
+
+std::mutex g_pipe_mu;
+std::unordered_map<int, std::unique_ptr<PipeCtx>> g_pipe;
+
+PipeCtx* pipe_ctx(int dev) {
+  std::lock_guard<std::mutex> lk(g_pipe_mu);
+  auto& p = g_pipe[dev];
+  if (!p) p = std::make_unique<PipeCtx>(dev);
+  return p->ok ? p.get() : nullptr;
+}
+
+bool host_is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+struct GatherSet {
+  unsigned long long src[kPipeMaxChunks];
+  unsigned long long len[kPipeMaxChunks];
+  unsigned long long dst[kPipeMaxChunks];
+};
+
+// blockIdx.y = chunk piece; copies the piece's keys of one slice into place.
+template <typename W>
+__global__ void k_gather(const W* a, W* b, GatherSet g) {
+  const int c = blockIdx.y;
+  const W* src = a + g.src[c];
+  W* dst = b + g.dst[c];
+  const unsigned long long len = g.len[c];
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < len;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+// Chunks / slices of the pipeline: VXSORT_HOST_CHUNKS=1 disables it (one
+// H2D, one device sort, one D2H).
+void pipe_dims(size_t n, size_t kb, int& C, int& S) {
+  const size_t bytes = n * kb;
+  C = bytes >= (size_t(64) << 20) ? 16 : 1;
+  S = bytes >= (size_t(256) << 20) ? 64 : 32;
+  if (const char* e = std::getenv("VXSORT_HOST_CHUNKS")) C = std::atoi(e);
+  if (const char* e = std::getenv("VXSORT_HOST_SLICES")) S = std::atoi(e);
+  C = std::max(1, std::min(C, kPipeMaxChunks));
+  int s2 = 2;
+  while (s2 * 2 <= std::min(std::max(S, 2), kPipeMaxSlices)) s2 *= 2;
+  S = s2;
+  if ((size_t)C * 4096 > n) C = 1;
+}
+
+// Chunk boundaries: equal chunks, then a geometric tail (1/2, 1/4, 1/8 of a
+// chunk) so the sort of the last chunk to land -- the only one not hidden
+// under the transfer -- is short.
+void chunk_bounds(size_t n, int C, ChunkSet& cs) {
+  cs.C = C;
+  double w[kPipeMaxChunks];
+  double tot = 0;
+  for (int c = 0; c < C; ++c) {
+    const int from_end = C - 1 - c;
+    w[c] = (C >= 6 && from_end < 3) ? 1.0 / (double)(1 << (3 - from_end)) : 1.0;  // 1/2, 1/4, 1/8
+    tot += w[c];
+  }
+  double acc = 0;
+  cs.off[0] = 0;
+  for (int c = 0; c < C; ++c) {
+    acc += w[c];
+    cs.off[c + 1] = c + 1 == C ? n : (unsigned long long)((double)n * acc / tot);
+  }
+}
+
+void add_stats(vxs_stats& acc, const vxs_stats& s) {
+  acc.max_depth = std::max(acc.max_depth, s.max_depth);
+  acc.partition_calls += s.partition_calls;
+  acc.base_case_calls += s.base_case_calls;
+  acc.keys_partitioned += s.keys_partitioned;
+  acc.fallback_triggered |= s.fallback_triggered;
+  acc.kernel_launches += s.kernel_launches;
+  acc.workspace_bytes = std::max(acc.workspace_bytes, s.workspace_bytes);
+}
+
+template <typename W>
+vxs_status host_pipeline(PipeCtx& X, W* h, size_t n, int xf, uint64_t seed, int C, int S, vxs_stats* stats) {
+  const int dev = X.dev;
+  const bool staged = !host_is_pinned(h);
+  if (staged && !X.ensure_staging()) return fail(VXS_OUT_OF_MEMORY, "vxsort_b200: pinned staging alloc failed");
+  const bool trace = std::getenv("VXSORT_PIPE_TRACE") != nullptr;
+  cudaEvent_t tev[6];  // start, H2D done, chunk sorts done, bounds done, first slice merged, D2H done
+  if (trace)
+    for (auto& t : tev) cudaEventCreate(&t);
+  vxs_stats acc{};
+  W *A = nullptr, *B = nullptr;
+  unsigned char* small = nullptr;
+  const size_t bounds_bytes = sizeof(unsigned long long) * C * (S + 1);
+  vxs_status st = VXS_OK;
+  cudaError_t e = cudaMallocAsync(&A, n * sizeof(W), X.s_cmp);
+  if (e == cudaSuccess) e = cudaMallocAsync(&B, n * sizeof(W), X.s_cmp);
+  if (e == cudaSuccess) e = cudaMallocAsync(&small, 256 + sizeof(W) * kPipeMaxSlices + bounds_bytes, X.s_cmp);
+  if (e != cudaSuccess) st = cuda_fail(e, "pipeline alloc");
+  W* spl = reinterpret_cast<W*>(small);
+  unsigned long long* d_bounds = reinterpret_cast<unsigned long long*>(small + 256 + sizeof(W) * kPipeMaxSlices);
+  cudaEventRecord(X.ev_alloc, X.s_cmp);
+  cudaStreamWaitEvent(X.s_in, X.ev_alloc, 0);
+  cudaStreamWaitEvent(X.s_out, X.ev_alloc, 0);
+  ChunkSet cs{};
+  chunk_bounds(n, C, cs);
+
+  // 1. chunked H2D on its own thread (a pageable source goes through the
+  //    pinned staging ring: parallel memcpy of piece i+1 overlaps the DMA of
+  //    piece i)
+  Ready in_ready, out_ready;
+  std::vector<unsigned long long> sl_off(S + 1, 0);
+  cudaError_t thread_err[2] = {cudaSuccess, cudaSuccess};
+  const bool ok_alloc = st == VXS_OK;
+  if (trace) cudaEventRecord(tev[0], X.s_in);
+  std::thread tin([&] {
+    cudaSetDevice(dev);
+    int piece = 0;
+    for (int c = 0; c < C; ++c) {
+      if (ok_alloc && thread_err[0] == cudaSuccess) {
+        const size_t b0 = cs.off[c] * sizeof(W), b1 = cs.off[c + 1] * sizeof(W);
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(h);
+        unsigned char* dst = reinterpret_cast<unsigned char*>(A);
+        if (!staged) {
+          const cudaError_t ce = cudaMemcpyAsync(dst + b0, src + b0, b1 - b0, cudaMemcpyHostToDevice, X.s_in);
+          if (ce != cudaSuccess) thread_err[0] = ce;
+        } else {
+          for (size_t p = b0; p < b1 && thread_err[0] == cudaSuccess; p += kStageBytes, ++piece) {
+            const int sl = piece % kStageSlots;
+            const size_t len = std::min(kStageBytes, b1 - p);
+            cudaEventSynchronize(X.ev_stage[sl]);  // slot's previous DMA done
+            X.pool->copy(X.slot(sl), src + p, len);
+            cudaError_t ce = cudaMemcpyAsync(dst + p, X.slot(sl), len, cudaMemcpyHostToDevice, X.s_in);
+            if (ce == cudaSuccess) ce = cudaEventRecord(X.ev_stage[sl], X.s_in);
+            if (ce != cudaSuccess) thread_err[0] = ce;
+          }
+        }
+      }
+      cudaEventRecord(X.ev_in[c], X.s_in);
+      if (trace && c == C - 1) cudaEventRecord(tev[1], X.s_in);
+      in_ready.post(c + 1);
+    }
+  });
+  // 3b. D2H of finished slices, in order (own thread for the same reason)
+  std::thread tout([&] {
+    cudaSetDevice(dev);
+    struct Pend {
+      int slot;
+      unsigned char* dst;
+      size_t len;
+    };
+    Pend q[kStageSlots];
+    int qh = 0, qn = 0, next = 0;
+    auto drain_one = [&] {
+      Pend& p = q[qh];
+      cudaEventSynchronize(X.ev_stage[kStageSlots + p.slot]);
+      X.pool->copy(p.dst, X.slot(kStageSlots + p.slot), p.len);
+      qh = (qh + 1) % kStageSlots;
+      --qn;
+    };
+    for (int s = 0; s < S; ++s) {
+      out_ready.wait(s + 1);
+      const unsigned long long len = sl_off[s + 1] - sl_off[s];
+      if (len == 0 || thread_err[1] != cudaSuccess) continue;
+      cudaStreamWaitEvent(X.s_out, X.ev_sl[s], 0);
+      if (!staged) {
+        const cudaError_t ce =
+            cudaMemcpyAsync(h + sl_off[s], B + sl_off[s], len * sizeof(W), cudaMemcpyDeviceToHost, X.s_out);
+        if (ce != cudaSuccess) thread_err[1] = ce;
+        continue;
+      }
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(B + sl_off[s]);
+      unsigned char* dst = reinterpret_cast<unsigned char*>(h + sl_off[s]);
+      for (size_t p = 0; p < (size_t)(len * sizeof(W)) && thread_err[1] == cudaSuccess; p += kStageBytes) {
+        if (qn == kStageSlots) drain_one();
+        const int sl = next;
+        next = (next + 1) % kStageSlots;
+        const size_t l = std::min(kStageBytes, (size_t)(len * sizeof(W)) - p);
+        cudaError_t ce = cudaMemcpyAsync(X.slot(kStageSlots + sl), src + p, l, cudaMemcpyDeviceToHost, X.s_out);
+        if (ce == cudaSuccess) ce = cudaEventRecord(X.ev_stage[kStageSlots + sl], X.s_out);
+        if (ce != cudaSuccess) {
+          thread_err[1] = ce;
+          break;
+        }
+        q[(qh + qn) % kStageSlots] = Pend{sl, dst + p, l};
+        ++qn;
+      }
+    }
+    while (qn) drain_one();
+  });
+  // 1b. sort each chunk as it lands
+  for (int c = 0; c < C; ++c) {
+    in_ready.wait(c + 1);
+    if (st != VXS_OK) continue;
+    cudaStreamWaitEvent(X.s_cmp, X.ev_in[c], 0);
+    vxs_stats sc{};
+    st = run_sort<W>(A + cs.off[c], cs.off[c + 1] - cs.off[c], xf, seed + (uint64_t)c * 0x9E3779B97F4A7C15ull,
+                     nullptr, 0, X.s_cmp, &sc);
+    add_stats(acc, sc);
+  }
+  // 2. global splitters from a regular sample of the sorted chunks; bounds
+  std::vector<unsigned long long> hb((size_t)C * (S + 1), 0);
+  if (trace) cudaEventRecord(tev[2], X.s_cmp);
+  if (st == VXS_OK) {
+    const size_t smem = (size_t)padded_size<W>(kPipeCand) * sizeof(W);
+    cudaFuncSetAttribute(k_pick_splitters<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_pick_splitters<W><<<1, 512, smem, X.s_cmp>>>(A, cs, xf, S, spl);
+    k_slice_bounds<W><<<(C * (S + 1) + 255) / 256, 256, 0, X.s_cmp>>>(A, cs, xf, S, spl, d_bounds);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hb.data(), d_bounds, bounds_bytes, cudaMemcpyDeviceToHost, X.s_cmp);
+    if (trace) cudaEventRecord(tev[3], X.s_cmp);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(X.s_cmp);
+    if (e != cudaSuccess) st = cuda_fail(e, "pipeline splitters");
+    acc.kernel_launches += 2;
+  }
+  // 3. per slice: merge the C sorted sub-runs (pairwise merge-path rounds,
+  //    no host sync; slices round-robin over kMergeStreams streams, each with
+  //    its own ping-pong buffer), hand the slice to the D2H thread
+  W* Tb = nullptr;
+  unsigned long long max_len = 0;
+  if (st == VXS_OK) {
+    for (int s = 0; s < S; ++s) {
+      unsigned long long len = 0;
+      for (int c = 0; c < C; ++c) len += hb[(size_t)c * (S + 1) + s + 1] - hb[(size_t)c * (S + 1) + s];
+      max_len = std::max(max_len, len);
+    }
+    max_len = std::max<unsigned long long>(max_len, 1);
+    e = cudaMallocAsync(&Tb, kMergeStreams * max_len * sizeof(W), X.s_cmp);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(X.s_cmp);
+    if (e != cudaSuccess) st = cuda_fail(e, "pipeline merge buffer");
+  }
+  constexpr int kMT = 256, kMI = 8, kMTile = kMT * kMI;
+  const size_t merge_smem = (size_t)padded_size<W>(kMTile) * sizeof(W);
+  int used_streams = 0;
+  for (int s = 0; s < S; ++s) {
+    unsigned long long len = 0;
+    Runs R{};
+    if (st == VXS_OK) {
+      for (int c = 0; c < C; ++c) {
+        const unsigned long long b0 = hb[(size_t)c * (S + 1) + s], b1 = hb[(size_t)c * (S + 1) + s + 1];
+        if (b1 == b0) continue;
+        R.src[R.m] = cs.off[c] + b0;
+        R.len[R.m] = b1 - b0;
+        ++R.m;
+        len += b1 - b0;
+      }
+    }
+    sl_off[s + 1] = sl_off[s] + len;
+    if (len) {
+      const int k = used_streams % kMergeStreams;
+      ++used_streams;
+      cudaStream_t ms = X.s_mrg[k];
+      W* tmp = Tb + (size_t)k * max_len;
+      if (R.m == 1) {
+        GatherSet g{};
+        g.src[0] = R.src[0];
+        g.len[0] = len;
+        g.dst[0] = sl_off[s];
+        const int gx = (int)std::min<unsigned long long>((len + 2047) / 2048, 1184);
+        k_gather<W><<<dim3(gx, 1), 256, 0, ms>>>(A, B, g);
+        acc.kernel_launches += 1;
+      } else {
+        int rounds = 0;
+        while ((1 << rounds) < R.m) ++rounds;
+        bool to_b = (rounds & 1) != 0;
+        const W* in = A;
+        const unsigned grid = (unsigned)((len + kMTile - 1) / kMTile);
+        for (int r = 0; r < rounds; ++r) {
+          W* out = to_b ? B + sl_off[s] : tmp;
+          k_merge_pairs<W, kMT, kMI><<<grid, kMT, merge_smem, ms>>>(in, R, out, xf);
+          acc.kernel_launches += 1;
+          Runs R2{};
+          R2.m = (R.m + 1) / 2;
+          unsigned long long pos = 0;
+          for (int j = 0; j < R2.m; ++j) {
+            R2.src[j] = pos;
+            R2.len[j] = R.len[2 * j] + (2 * j + 1 < R.m ? R.len[2 * j + 1] : 0ull);
+            pos += R2.len[j];
+          }
+          R = R2;
+          in = out;
+          to_b = !to_b;
+        }
+      }
+      e = cudaGetLastError();
+      if (e != cudaSuccess && st == VXS_OK) st = cuda_fail(e, "pipeline merge");
+      cudaEventRecord(X.ev_sl[s], ms);
+      if (trace && sl_off[s] == 0) cudaEventRecord(tev[4], ms);
+    }
+    out_ready.post(s + 1);
+  }
+  tin.join();
+  tout.join();
+  // frees are ordered after the merges and the D2H copies
+  for (int k = 0; k < kMergeStreams; ++k) {
+    cudaEventRecord(X.ev_mrg[k], X.s_mrg[k]);
+    cudaStreamWaitEvent(X.s_cmp, X.ev_mrg[k], 0);
+  }
+  cudaEventRecord(X.ev_done, X.s_out);
+  if (trace) {
+    cudaEventRecord(tev[5], X.s_out);
+    cudaEventSynchronize(tev[5]);
+    float t[6] = {};
+    for (int i = 1; i < 6; ++i) cudaEventElapsedTime(&t[i], tev[0], tev[i]);
+    std::fprintf(stderr,
+                 "[vxsort pipe C=%d S=%d %s] h2d %.3f  chunk-sorts %.3f  bounds %.3f  slice0 %.3f  d2h-done %.3f ms\n",
+                 C, S, staged ? "staged" : "pinned", t[1], t[2], t[3], t[4], t[5]);
+    for (auto& x : tev) cudaEventDestroy(x);
+  }
+  cudaStreamWaitEvent(X.s_cmp, X.ev_done, 0);
+  if (A) cudaFreeAsync(A, X.s_cmp);
+  if (B) cudaFreeAsync(B, X.s_cmp);
+  if (small) cudaFreeAsync(small, X.s_cmp);
+  if (Tb) cudaFreeAsync(Tb, X.s_cmp);
+  e = cudaStreamSynchronize(X.s_cmp);
+  if (st == VXS_OK && e != cudaSuccess) st = cuda_fail(e, "pipeline sync");
+  if (st == VXS_OK && thread_err[0] != cudaSuccess) st = cuda_fail(thread_err[0], "H2D");
+  if (st == VXS_OK && thread_err[1] != cudaSuccess) st = cuda_fail(thread_err[1], "D2H");
+  if (st == VXS_OK && sl_off[S] != n) st = fail(VXS_INTERNAL, "vxsort_b200: pipeline slices do not cover the input");
+  if (stats) {
+    acc.max_depth += 1;  // the slice merge stage
+    acc.workspace_bytes += (2 * n + kMergeStreams * max_len) * sizeof(W);
+    *stats = acc;
+  }
+  return st;
 }
 
 }  // namespace
@@ -529,6 +1044,22 @@ vxs_status vxs_sort_host(void* h_keys, size_t n, vxs_key_type type, vxs_order or
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_mu);
     ensure_pool(dev, g_dev[dev]);
+  }
+  {
+    int C = 1, S = 2;
+    pipe_dims(n, kb, C, S);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    PipeCtx* X = C > 1 ? pipe_ctx(dev) : nullptr;
+    if (X) {
+      const int xf = xform_for(type, order);
+      const uint64_t sd = seed_for(seed, has_seed, h_keys, n);
+      std::lock_guard<std::mutex> lk(X->busy);
+      return with_word(type, [&](auto* tag) {
+        using W = std::remove_pointer_t<decltype(tag)>;
+        return host_pipeline<W>(*X, static_cast<W*>(h_keys), n, xf, sd, C, S, stats);
+      });
+    }
   }
   cudaStream_t st;
   VXS_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream create");
