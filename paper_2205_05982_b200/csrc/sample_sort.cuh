@@ -1038,10 +1038,10 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       if (X.flt) classify_tile(std::integral_constant<int, 0>{}, std::true_type{});
       else classify_tile(std::integral_constant<int, 0>{}, std::false_type{});
     }
-    while (wide) {
-      const int i = __ffs(wide) - 1;
-      wide &= wide - 1;
-      bk[i] = classify_slow(k[i], S);
+    if (wide) {  // rare; static indices keep k[] / bk[] in registers
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i)
+        if (bk[i] == -1) bk[i] = classify_slow(k[i], S);
     }
     // rank within (warp, child); bk[] becomes child << 16 | rank
     bool same = bk[0] >= 0;
