@@ -54,10 +54,7 @@ __device__ __forceinline__ void warp_bitonic_merge(W (&k)[N], int lane) {
 #pragma unroll
       for (int i = 0; i < N; ++i) other[i] = shfl_xor(k[N - 1 - i], lane_mask);
 #pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const bool lt = key_lt(other[i], k[i]);
-        if (lower ? lt : !lt) k[i] = other[i];
-      }
+      for (int i = 0; i < N; ++i) k[i] = keep_minmax(k[i], other[i], lower);
     }
     // Half-cleaner steps with strides size/4 ... 1 (in keys).
 #pragma unroll
@@ -65,12 +62,9 @@ __device__ __forceinline__ void warp_bitonic_merge(W (&k)[N], int lane) {
       if (stride >= N) {
         const int lx = stride / N;
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-          W other = shfl_xor(k[i], lx);
-          const bool lower = (lane & lx) == 0;
-          const bool lt = key_lt(other, k[i]);
-          if (lower ? lt : !lt) k[i] = other;
-        }
+        const bool lower = (lane & lx) == 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) k[i] = keep_minmax(k[i], shfl_xor(k[i], lx), lower);
       } else {
 #pragma unroll
         for (int i = 0; i < N; ++i) {
@@ -86,7 +80,7 @@ __device__ __forceinline__ void warp_bitonic_merge(W (&k)[N], int lane) {
 // accesses (lane stride ITEMS) and merge-path windows hit distinct banks.
 template <typename W>
 __host__ __device__ constexpr int pad_idx(int i) {
-  return i + i / (128 / (int)sizeof(W));
+  return (int)((unsigned)i + (unsigned)i / (128u / (unsigned)sizeof(W)));  // i >= 0: shift, no sign fixup
 }
 template <typename W>
 __host__ __device__ constexpr int padded_size(int n) {

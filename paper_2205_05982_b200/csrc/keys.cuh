@@ -187,6 +187,24 @@ __device__ __forceinline__ void cas(W& a, W& b) {
   b = hi;
 }
 
+// Half-cleaner step against a partner value: keep the smaller key when
+// take_min, else the larger.  For 32/16-bit words this is one predicated
+// integer min/max (VIMNMX with a lane-dependent predicate), not a compare +
+// select.
+template <typename W>
+__device__ __forceinline__ W keep_minmax(const W& k, const W& other, bool take_min) {
+  const bool lt = key_lt(other, k);
+  return (take_min ? lt : !lt) ? other : k;
+}
+template <>
+__device__ __forceinline__ uint32_t keep_minmax<uint32_t>(const uint32_t& k, const uint32_t& other, bool take_min) {
+  return take_min ? umin(k, other) : umax(k, other);
+}
+template <>
+__device__ __forceinline__ uint16_t keep_minmax<uint16_t>(const uint16_t& k, const uint16_t& other, bool take_min) {
+  return (uint16_t)(take_min ? umin((unsigned)k, (unsigned)other) : umax((unsigned)k, (unsigned)other));
+}
+
 // ---- transforms -----------------------------------------------------------
 template <typename W>
 __host__ __device__ __forceinline__ W flt_enc(W b, bool desc) {
