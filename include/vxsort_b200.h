@@ -88,6 +88,27 @@ vxs_status vxs_sort(void* d_keys, size_t n, vxs_key_type type, vxs_order order, 
 vxs_status vxs_sort_host(void* h_keys, size_t n, vxs_key_type type, vxs_order order, uint64_t seed,
                          int has_seed, vxs_stats* stats);
 
+/* Stable argsort and key+value sort (the row-id trick of
+ * "appending a unique row identifier to the least
+ * significant bits" -- applied on the device).  Each key is packed with its
+ * index into one wider word (64-bit for 16/32-bit keys while n <= 2^32,
+ * 128-bit {lo = index, hi = key} otherwise and for 64-bit keys) and the
+ * packed words are sorted; ties therefore keep ascending index order in
+ * both directions (a stable sort).  128-bit keys (K128/KV64) are not
+ * supported (VXS_INVALID_ARGUMENT).
+ * vxs_argsort: d_indices[i] = original position of the i-th key in sorted
+ *   order; if d_sorted_keys is non-NULL it receives the sorted keys.  d_keys
+ *   is not modified.
+ * vxs_sort_pairs: sorts d_keys in place and permutes d_values (n elements of
+ *   value_bytes = 1, 2, 4, 8 or 16) alongside. */
+vxs_status vxs_argsort_workspace_bytes(size_t n, vxs_key_type type, size_t value_bytes, size_t* bytes);
+vxs_status vxs_argsort(const void* d_keys, size_t n, vxs_key_type type, vxs_order order, uint64_t* d_indices,
+                       void* d_sorted_keys, uint64_t seed, int has_seed, void* d_workspace,
+                       size_t workspace_bytes, void* stream, vxs_stats* stats);
+vxs_status vxs_sort_pairs(void* d_keys, void* d_values, size_t value_bytes, size_t n, vxs_key_type type,
+                          vxs_order order, uint64_t seed, int has_seed, void* d_workspace,
+                          size_t workspace_bytes, void* stream, vxs_stats* stats);
+
 /* Distributed sample sort building blocks.
  * vxs_sample: s stratified random samples of d_keys written to d_out as
  *   ORDER-TRANSFORMED unsigned words of the key width (sortable as unsigned).

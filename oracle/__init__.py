@@ -190,3 +190,28 @@ def canonical_sorted(keys: np.ndarray, key_type: str, descending: bool = False) 
         return np.concatenate([bb[o], nanbits]).view(a.dtype)
     s = np.sort(a, kind="stable")
     return s[::-1].copy() if descending else s
+
+
+def canonical_argsort(keys: np.ndarray, key_type: str, descending: bool = False) -> np.ndarray:
+    """Stable argsort in the canonical order (test oracle for vxs_argsort /
+    vxs_sort_pairs, SURVEY §8 f2 + §8c.3): keys by the canonical total order
+    (floats: IEEE totalOrder on non-NaN, NaN last in both orders, NaNs by raw
+    bits), ties by ascending original index in both orders -- i.e. the
+    order of the packed (key, row id) words of PAPER.md:907-910."""
+    a = np.ascontiguousarray(keys)
+    n = a.shape[0]
+    idx = np.arange(n, dtype=np.int64)
+    nbits = 8 * a.itemsize
+    ut = {2: np.uint16, 4: np.uint32, 8: np.uint64}[a.itemsize]
+    u = a.view(ut)
+    top = ut(1) << ut(nbits - 1)
+    if key_type in ("f32", "f64"):
+        isnan = np.isnan(a)
+        sign = (u & top) != 0
+        tk = np.where(sign, ~u, u | top).astype(ut)
+        prim = np.where(isnan, u, ~tk if descending else tk).astype(ut)
+        return np.lexsort((idx, prim, isnan.astype(np.uint8)))
+    if key_type in ("i16", "i32", "i64"):
+        u = (u ^ top).astype(ut)
+    prim = ~u if descending else u
+    return np.lexsort((idx, prim))

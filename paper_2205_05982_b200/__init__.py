@@ -134,15 +134,20 @@ def lib():
         L.vxs_profile_enable.argtypes = [i]
         L.vxs_profile_read.argtypes = [ctypes.c_void_p, i]
         L.vxs_profile_read.restype = i
+        L.vxs_argsort_workspace_bytes.argtypes = [sz, i, sz, ctypes.POINTER(ctypes.c_size_t)]
+        L.vxs_argsort.argtypes = [vp, sz, i, i, vp, vp, u64, i, vp, sz, vp, ctypes.POINTER(SortStats)]
+        L.vxs_sort_pairs.argtypes = [vp, vp, sz, sz, i, i, u64, i, vp, sz, vp, ctypes.POINTER(SortStats)]
         for fn in ("vxs_sort", "vxs_sort_host", "vxs_sort_workspace_bytes", "vxs_sample",
-                   "vxs_partition", "vxs_transform"):
+                   "vxs_partition", "vxs_transform", "vxs_argsort_workspace_bytes", "vxs_argsort",
+                   "vxs_sort_pairs"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
 
 
 EXPORTED_SYMBOLS = ["vxs_sort_workspace_bytes", "vxs_sort", "vxs_sort_host", "vxs_sample",
-                    "vxs_partition", "vxs_transform", "vxs_last_error", "vxs_key_bytes",
+                    "vxs_partition", "vxs_transform", "vxs_argsort_workspace_bytes", "vxs_argsort",
+                    "vxs_sort_pairs", "vxs_last_error", "vxs_key_bytes",
                     "vxs_base_case_capacity", "vxs_version", "vxs_profile_enable",
                     "vxs_profile_reset", "vxs_profile_read"]
 
@@ -249,6 +254,59 @@ def sort(keys, config: Optional[SortConfig] = None, key_type: Optional[str] = No
         raise ValueError("host keys must be a writeable C-contiguous numpy array")
     _check(lib().vxs_sort_host(arr.ctypes.data, n, KEY_CODE[kt], int(cfg.order), seed, has_seed,
                                ctypes.byref(st)))
+    return st
+
+
+def argsort_workspace_bytes(n: int, key_type: str, value_bytes: int = 0) -> int:
+    out = ctypes.c_size_t()
+    _check(lib().vxs_argsort_workspace_bytes(n, KEY_CODE[key_type], value_bytes, ctypes.byref(out)))
+    return out.value
+
+
+def _seed_args(seed):
+    return (0, 0) if seed is None else (int(seed) & (2**64 - 1), 1)
+
+
+def argsort(keys, order: Order = Order.kAscending, key_type: Optional[str] = None, sorted_keys=None,
+            workspace=None, stream=None, seed: Optional[int] = None):
+    """Stable argsort of device keys: int64 indices such that
+    keys[idx] is sorted; ties keep ascending index in both orders.  Optionally
+    writes the sorted keys into ``sorted_keys``.  ``keys`` is not modified."""
+    import torch
+    kt = infer_key_type(keys, key_type)
+    if not (_is_torch(keys) and keys.is_cuda and keys.is_contiguous()):
+        raise ValueError("argsort takes a contiguous CUDA tensor")
+    n = _nkeys(keys, kt)
+    idx = torch.empty(n, dtype=torch.int64, device=keys.device)
+    ws_ptr, ws_n = (None, 0) if workspace is None else (workspace.data_ptr(),
+                                                       workspace.numel() * workspace.element_size())
+    sd, has = _seed_args(seed)
+    st = SortStats()
+    _check(lib().vxs_argsort(keys.data_ptr(), n, KEY_CODE[kt], int(order), idx.data_ptr(),
+                             None if sorted_keys is None else sorted_keys.data_ptr(), sd, has, ws_ptr, ws_n,
+                             _stream_ptr(stream), ctypes.byref(st)))
+    return idx
+
+
+def sort_pairs(keys, values, config: Optional[SortConfig] = None, key_type: Optional[str] = None,
+               workspace=None, stream=None) -> SortStats:
+    """Sort device keys in place and permute ``values`` (same length, any
+    element size of 1/2/4/8/16 bytes per key) alongside, stably (§8 f2)."""
+    cfg = config or SortConfig()
+    kt = infer_key_type(keys, key_type)
+    for t in (keys, values):
+        if not (_is_torch(t) and t.is_cuda and t.is_contiguous()):
+            raise ValueError("sort_pairs takes contiguous CUDA tensors")
+    n = _nkeys(keys, kt)
+    if values.shape[0] != n:
+        raise ValueError("values must have one row per key")
+    vb = values.numel() * values.element_size() // max(n, 1) if n else values.element_size()
+    ws_ptr, ws_n = (None, 0) if workspace is None else (workspace.data_ptr(),
+                                                       workspace.numel() * workspace.element_size())
+    sd, has = _seed_args(cfg.seed)
+    st = SortStats()
+    _check(lib().vxs_sort_pairs(keys.data_ptr(), values.data_ptr(), vb, n, KEY_CODE[kt], int(cfg.order), sd, has,
+                                ws_ptr, ws_n, _stream_ptr(stream), ctypes.byref(st)))
     return st
 
 

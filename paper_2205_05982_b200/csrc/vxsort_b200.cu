@@ -939,6 +939,127 @@ vxs_status host_pipeline(PipeCtx& X, W* h, size_t n, int xf, uint64_t seed, int 
   return st;
 }
 
+// ---- stable argsort / key+value sort ------------------------
+// Key and index packed into one word (PAPER.md:907-910 row-id trick): the
+// packed words are distinct, so the sort is stable by construction.
+
+__device__ __forceinline__ void pack_kv(unsigned long long& p, unsigned long long k, unsigned long long i) {
+  p = (k << 32) | i;
+}
+__device__ __forceinline__ void pack_kv(U128& p, unsigned long long k, unsigned long long i) { p = U128{i, k}; }
+__device__ __forceinline__ unsigned long long packed_idx(const unsigned long long& p) { return p & 0xFFFFFFFFull; }
+__device__ __forceinline__ unsigned long long packed_idx(const U128& p) { return p.lo; }
+__device__ __forceinline__ unsigned long long packed_key(const unsigned long long& p) { return p >> 32; }
+__device__ __forceinline__ unsigned long long packed_key(const U128& p) { return p.hi; }
+
+template <typename WK, typename WP>
+__global__ void k_pack_index(const WK* keys, WP* out, unsigned long long n, int xf) {
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    WP p;
+    pack_kv(p, (unsigned long long)enc<WK>(ldcs(keys + i), xf), i);
+    out[i] = p;
+  }
+}
+
+template <typename WK, typename WP, typename V>
+__global__ void k_unpack_index(const WP* packed, unsigned long long n, int xf, unsigned long long* idx_out,
+                               WK* keys_out, const V* vals_in, V* vals_out) {
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const WP p = packed[i];
+    const unsigned long long j = packed_idx(p);
+    if (idx_out) idx_out[i] = j;
+    if (keys_out) keys_out[i] = dec<WK>((WK)packed_key(p), xf);
+    if (vals_out) vals_out[i] = vals_in[j];
+  }
+}
+
+bool pack_wide(size_t n, size_t kb) { return kb >= 8 || n > (size_t(1) << 32); }
+
+struct PackLayout {
+  size_t packed, sort_ws, sort_ws_bytes, vals, total;
+};
+
+PackLayout pack_layout(size_t n, size_t kb, size_t vb) {
+  PackLayout L{};
+  const bool wide = pack_wide(n, kb);
+  size_t off = 0;
+  L.packed = off;
+  off = align_up(off + n * (wide ? 16 : 8), 256);
+  L.sort_ws = off;
+  L.sort_ws_bytes = wide ? layout_for<U128>(n).total : layout_for<unsigned long long>(n).total;
+  off = align_up(off + L.sort_ws_bytes, 256);
+  L.vals = off;
+  off = align_up(off + n * vb, 256);
+  L.total = off;
+  return L;
+}
+
+bool valid_value_bytes(size_t vb) { return vb == 1 || vb == 2 || vb == 4 || vb == 8 || vb == 16; }
+
+template <class F>
+vxs_status with_value(size_t vb, F&& f) {
+  switch (vb) {
+    case 1: return f((uint8_t*)nullptr);
+    case 2: return f((uint16_t*)nullptr);
+    case 4: return f((uint32_t*)nullptr);
+    case 8: return f((unsigned long long*)nullptr);
+    case 16: return f((U128*)nullptr);
+  }
+  return f((uint8_t*)nullptr);
+}
+
+// keys_in -> (idx_out?, keys_out?, values permuted in place?)
+template <typename WK, typename WP, typename V>
+vxs_status run_packed(const WK* keys_in, size_t n, int xf, uint64_t seed, unsigned long long* idx_out, WK* keys_out,
+                      V* vals, size_t vb, void* ws, size_t ws_bytes, cudaStream_t st, vxs_stats* stats) {
+  const PackLayout L = pack_layout(n, sizeof(WK), vals ? vb : 0);
+  void* owned = nullptr;
+  if (ws == nullptr) {
+    VXS_CK(cudaMallocAsync(&owned, std::max<size_t>(L.total, 256), st), "workspace alloc");
+    ws = owned;
+  } else if (ws_bytes < L.total) {
+    return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: provided workspace is too small");
+  }
+  unsigned char* base = static_cast<unsigned char*>(ws);
+  WP* packed = reinterpret_cast<WP*>(base + L.packed);
+  V* vtmp = reinterpret_cast<V*>(base + L.vals);
+  const int g = (int)std::min<size_t>((n + 255) / 256, 148 * 16);
+  {
+    ProfScope ps(K_MISC, st);
+    k_pack_index<WK, WP><<<g, 256, 0, st>>>(keys_in, packed, n, xf);
+  }
+  VXS_CK(cudaGetLastError(), "pack");
+  vxs_status s = run_sort<WP>(packed, n, XF_NONE, seed, base + L.sort_ws, L.sort_ws_bytes, st, stats);
+  if (s != VXS_OK) {
+    if (owned) cudaFreeAsync(owned, st);
+    return s;
+  }
+  {
+    ProfScope ps(K_MISC, st);
+    k_unpack_index<WK, WP, V><<<g, 256, 0, st>>>(packed, n, xf, idx_out, keys_out, vals, vals ? vtmp : nullptr);
+  }
+  VXS_CK(cudaGetLastError(), "unpack");
+  if (vals) VXS_CK(cudaMemcpyAsync(vals, vtmp, n * vb, cudaMemcpyDeviceToDevice, st), "values copy");
+  if (owned) VXS_CK(cudaFreeAsync(owned, st), "workspace free");
+  if (stats) {
+    stats->kernel_launches += 2;
+    stats->workspace_bytes = L.total;
+  }
+  return VXS_OK;
+}
+
+template <typename WK, typename V>
+vxs_status dispatch_packed(const WK* keys_in, size_t n, int xf, uint64_t seed, unsigned long long* idx_out,
+                           WK* keys_out, V* vals, size_t vb, void* ws, size_t ws_bytes, cudaStream_t st,
+                           vxs_stats* stats) {
+  if (pack_wide(n, sizeof(WK)))
+    return run_packed<WK, U128, V>(keys_in, n, xf, seed, idx_out, keys_out, vals, vb, ws, ws_bytes, st, stats);
+  return run_packed<WK, unsigned long long, V>(keys_in, n, xf, seed, idx_out, keys_out, vals, vb, ws, ws_bytes, st,
+                                               stats);
+}
+
 }  // namespace
 }  // namespace vxs
 
@@ -1083,6 +1204,70 @@ vxs_status vxs_sort_host(void* h_keys, size_t n, vxs_key_type type, vxs_order or
   cudaStreamDestroy(st);
   if (stats) stats->kernel_launches += 0;
   return s;
+}
+
+vxs_status vxs_argsort_workspace_bytes(size_t n, vxs_key_type type, size_t value_bytes, size_t* bytes) {
+  if (!bytes) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: bytes is NULL");
+  const size_t kb = (size_t)word_bytes(type);
+  if (kb == 0 || kb == 16) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: argsort supports 16/32/64-bit keys");
+  if (value_bytes && !valid_value_bytes(value_bytes))
+    return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: value_bytes must be 1, 2, 4, 8 or 16");
+  *bytes = pack_layout(n, kb, value_bytes).total;
+  return VXS_OK;
+}
+
+vxs_status vxs_argsort(const void* d_keys, size_t n, vxs_key_type type, vxs_order order, uint64_t* d_indices,
+                       void* d_sorted_keys, uint64_t seed, int has_seed, void* d_workspace, size_t workspace_bytes,
+                       void* stream, vxs_stats* stats) {
+  if (!valid_order(order)) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: invalid order");
+  const size_t kb = (size_t)word_bytes(type);
+  if (kb == 0 || kb == 16) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: argsort supports 16/32/64-bit keys");
+  if (n > 0 && (d_keys == nullptr || d_indices == nullptr))
+    return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: keys/indices is NULL");
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  if (n == 0) return VXS_OK;
+  const int xf = xform_for(type, order);
+  const uint64_t sd = seed_for(seed, has_seed, d_keys, n);
+  return with_word(type, [&](auto* tag) -> vxs_status {
+    using WK = std::remove_pointer_t<decltype(tag)>;
+    if constexpr (sizeof(WK) == 16) {
+      return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: argsort supports 16/32/64-bit keys");
+    } else {
+      return dispatch_packed<WK, uint8_t>(static_cast<const WK*>(d_keys), n, xf, sd,
+                                          reinterpret_cast<unsigned long long*>(d_indices),
+                                          static_cast<WK*>(d_sorted_keys), nullptr, 0, d_workspace, workspace_bytes,
+                                          static_cast<cudaStream_t>(stream), stats);
+    }
+  });
+}
+
+vxs_status vxs_sort_pairs(void* d_keys, void* d_values, size_t value_bytes, size_t n, vxs_key_type type,
+                          vxs_order order, uint64_t seed, int has_seed, void* d_workspace, size_t workspace_bytes,
+                          void* stream, vxs_stats* stats) {
+  if (!valid_order(order)) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: invalid order");
+  const size_t kb = (size_t)word_bytes(type);
+  if (kb == 0 || kb == 16) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: sort_pairs supports 16/32/64-bit keys");
+  if (!valid_value_bytes(value_bytes))
+    return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: value_bytes must be 1, 2, 4, 8 or 16");
+  if (n > 0 && (d_keys == nullptr || d_values == nullptr))
+    return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: keys/values is NULL");
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  if (n <= 1) return VXS_OK;
+  const int xf = xform_for(type, order);
+  const uint64_t sd = seed_for(seed, has_seed, d_keys, n);
+  return with_word(type, [&](auto* tag) -> vxs_status {
+    using WK = std::remove_pointer_t<decltype(tag)>;
+    if constexpr (sizeof(WK) == 16) {
+      return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: sort_pairs supports 16/32/64-bit keys");
+    } else {
+      return with_value(value_bytes, [&](auto* vtag) -> vxs_status {
+        using V = std::remove_pointer_t<decltype(vtag)>;
+        return dispatch_packed<WK, V>(static_cast<const WK*>(d_keys), n, xf, sd, nullptr, static_cast<WK*>(d_keys),
+                                      static_cast<V*>(d_values), value_bytes, d_workspace, workspace_bytes,
+                                      static_cast<cudaStream_t>(stream), stats);
+      });
+    }
+  });
 }
 
 vxs_status vxs_transform(void* d_keys, size_t n, vxs_key_type type, vxs_order order, int inverse, void* stream) {

@@ -185,3 +185,23 @@ class TestAgainstRealReference:
         x = np.ones(10, np.uint64)
         assert oracle.ref().ref_sort_with_scratch(x.ctypes.data, 10, oracle.KEY_CODE["u64"], 16) == 1
         assert oracle.ref().ref_scratch_bytes(oracle.KEY_CODE["u64"]) == 2048
+
+
+@pytest.mark.parametrize("kt", ["i16", "u16", "i32", "u32", "f32", "i64", "u64", "f64"])
+def test_canonical_argsort_consistent_with_canonical_sort(kt):
+    """The stable-argsort oracle (§8 f2) permutes keys into exactly the
+    canonical sorted order, and is stable (ties by ascending index)."""
+    rng = np.random.default_rng(3)
+    dt = {"i16": np.int16, "u16": np.uint16, "i32": np.int32, "u32": np.uint32, "f32": np.float32,
+          "i64": np.int64, "u64": np.uint64, "f64": np.float64}[kt]
+    if kt in ("f32", "f64"):
+        x = (rng.standard_normal(5000) * 10).round().astype(dt)
+        x[::7] = np.array([-0.0, 0.0, np.inf, -np.inf, np.nan], dt)[np.arange(len(x[::7])) % 5]
+    else:
+        x = rng.integers(0, 50, 5000).astype(dt)
+    for desc in (False, True):
+        o = oracle.canonical_argsort(x, kt, desc)
+        assert x[o].tobytes() == oracle.canonical_sorted(x, kt, desc).tobytes()
+        same = x[o][1:].view(np.uint8).reshape(len(x) - 1, -1) == x[o][:-1].view(np.uint8).reshape(len(x) - 1, -1)
+        ties = same.all(axis=1)
+        assert np.all(o[1:][ties] > o[:-1][ties])
