@@ -171,6 +171,31 @@ SortStats sort_device(T* d_keys, std::size_t n, const SortConfig& config = {}, v
   return detail::to_stats(st);
 }
 
+// Extensions beyond the reference surface: stable argsort and
+// key+value sort of device-resident keys (16/32/64-bit key types).
+template <typename T>
+SortStats argsort_device(const T* d_keys, std::size_t n, std::uint64_t* d_indices, T* d_sorted_keys = nullptr,
+                         const SortConfig& config = {}, void* stream = nullptr, void* d_workspace = nullptr,
+                         std::size_t workspace_bytes = 0) {
+  vxs_stats st{};
+  detail::throw_status(vxs_argsort(d_keys, n, detail::KeyCode<T>::v,
+                                   config.order == Order::kAscending ? VXS_ASCENDING : VXS_DESCENDING, d_indices,
+                                   d_sorted_keys, config.seed.value_or(0), config.seed.has_value() ? 1 : 0,
+                                   d_workspace, workspace_bytes, stream, &st));
+  return detail::to_stats(st);
+}
+
+template <typename T, typename V>
+SortStats sort_pairs_device(T* d_keys, V* d_values, std::size_t n, const SortConfig& config = {},
+                            void* stream = nullptr, void* d_workspace = nullptr, std::size_t workspace_bytes = 0) {
+  vxs_stats st{};
+  detail::throw_status(vxs_sort_pairs(d_keys, d_values, sizeof(V), n, detail::KeyCode<T>::v,
+                                      config.order == Order::kAscending ? VXS_ASCENDING : VXS_DESCENDING,
+                                      config.seed.value_or(0), config.seed.has_value() ? 1 : 0, d_workspace,
+                                      workspace_bytes, stream, &st));
+  return detail::to_stats(st);
+}
+
 // The B200 path is data-parallel device code; kept for source compatibility
 // with vexsort.hpp:132.
 inline bool wide_backend_is_simd() { return true; }

@@ -79,3 +79,52 @@ def test_cpp_header_mirrors_reference_surface():
     for name in ("struct SortConfig", "class SortScratch", "scratch_bytes", "enum class Order",
                  "enum class Backend", "wide_backend_is_simd"):
         assert name in hpp
+
+
+def test_cpp_dropin_compiles_links_and_runs(tmp_path):
+    """INTEGRATION.md's recompile-only drop-in: a reference-style call site
+    (harness.cpp:264 / test_driver.cpp style) compiles against
+    include/vexsort_b200.hpp, links libvxsort_b200.so, and runs the
+    device-free paths (n <= 1, too-small scratch -> std::invalid_argument)."""
+    import shutil
+    import subprocess
+    if shutil.which("g++") is None:
+        pytest.skip("no g++")
+    src = tmp_path / "dropin.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include <vector>
+#include "vexsort_b200.hpp"
+int main() {
+  std::vector<std::uint64_t> one{42};
+  vexsort::SortStats st = vexsort::sort(std::span<std::uint64_t>(one), vexsort::SortConfig{});
+  if (st.max_depth != 0 || one[0] != 42) return 1;
+  std::vector<float> none;
+  vexsort::sort(std::span<float>(none));
+  std::vector<vexsort::K128> k(1);
+  vexsort::sort(std::span<vexsort::K128>(k), vexsort::SortConfig{.order = vexsort::Order::kDescending});
+  vexsort::SortScratch small(16);
+  std::vector<std::int32_t> v{3, 1, 2};
+  try {
+    vexsort::SortConfig cfg;
+    cfg.scratch = &small;
+    vexsort::sort(std::span<std::int32_t>(v), cfg);
+    return 2;
+  } catch (const std::invalid_argument&) {
+  }
+  if (false) {  // instantiate the device-pointer entry points
+    vexsort::sort_device<std::uint32_t>(nullptr, 0);
+    vexsort::argsort_device<std::uint32_t>(nullptr, 0, nullptr);
+    vexsort::sort_pairs_device<std::int64_t, double>(nullptr, nullptr, 0);
+  }
+  std::puts("ok");
+  return 0;
+}
+''')
+    exe = tmp_path / "dropin"
+    lib_dir = os.path.join(ROOT, "paper_2205_05982_b200", "lib")
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+                        "-L", lib_dir, "-lvxsort_b200", f"-Wl,-rpath,{lib_dir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", (r.returncode, r.stdout, r.stderr)
