@@ -345,7 +345,10 @@ def run_single(args):
     if ncu and ncu.get("workload") == args.workload and dom_name in ncu.get("kernels", {}):
         traffic = ncu["kernels"][dom_name].get("dram_bytes_per_launch")
     total_alg = algorithmic_bytes(st, n, kb)["total"]
-    e2e_t, hbytes = e2e_host(x, kt, desc, min(steps, 5))
+    if args.no_e2e:  # profiling runs only: keep the launch list to the device-resident sort
+        e2e_t, hbytes = [float("nan")], 0
+    else:
+        e2e_t, hbytes = e2e_host(x, kt, desc, min(steps, 5))
     e2e_s = statistics.median(e2e_t)
     line = {
         "metric": "Mkeys/s sorted (in-memory key sort)",
@@ -514,6 +517,7 @@ def main():
     ap.add_argument("--extras", default="u64-uniform,c2-f32-asc")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-API e2e leg (ncu launch lists only)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -42,7 +42,7 @@ for r in rows:
 tot = sum(v[1] for v in per.values())
 with open(os.path.join(out_dir, f"{tag}_launches.md"), "w") as f:
     f.write(f"# {tag}: ncu launch list (`--metrics gpu__time_duration.sum --clock-control none`)\n\n")
-    f.write(f"Command: `python bench.py --steps 2 --warmup 1 --no-extras --no-cpu` (workload {workload}).\n")
+    f.write(f"Command: `python bench.py --steps 2 --warmup 3 --no-extras --no-cpu --no-e2e` (workload {workload}).\n")
     f.write("Times are cold-cache and serialised by ncu; compare shares, not absolutes.\n\n")
     f.write("| kernel | launches | total us | share |\n|---|---|---|---|\n")
     for k, (n, us) in sorted(per.items(), key=lambda kv: -kv[1][1]):
