@@ -88,6 +88,20 @@ vxs_status vxs_sort(void* d_keys, size_t n, vxs_key_type type, vxs_order order, 
 vxs_status vxs_sort_host(void* h_keys, size_t n, vxs_key_type type, vxs_order order, uint64_t seed,
                          int has_seed, vxs_stats* stats);
 
+/* Partial sort / selection (std::nth_element and
+ * std::partial_sort semantics, generalised to an output range): after the
+ * call d_keys[lo, hi) holds, sorted, exactly the keys of sorted ranks
+ * lo..hi-1; every key before lo precedes (or equals) them and every key from
+ * hi on follows (or equals) them in the requested order; d_keys stays a
+ * permutation of the input.  Buckets whose final range misses [lo, hi) are
+ * never split or sorted -- they are only moved back into place -- so
+ * selecting one rank costs one multiway pass plus the narrowing levels.
+ * nth_element(k) = [k, k+1); top-k / partial_sort(k) = [0, k).  Requires
+ * lo <= hi <= n (lo == hi: no-op).  Workspace as vxs_sort_workspace_bytes. */
+vxs_status vxs_sort_range(void* d_keys, size_t n, vxs_key_type type, vxs_order order, size_t lo, size_t hi,
+                          uint64_t seed, int has_seed, void* d_workspace, size_t workspace_bytes, void* stream,
+                          vxs_stats* stats);
+
 /* Stable argsort and key+value sort (the row-id trick of
  * "appending a unique row identifier to the least
  * significant bits" -- applied on the device).  Each key is packed with its

@@ -134,6 +134,8 @@ def lib():
         L.vxs_profile_enable.argtypes = [i]
         L.vxs_profile_read.argtypes = [ctypes.c_void_p, i]
         L.vxs_profile_read.restype = i
+        L.vxs_sort_range.argtypes = [vp, sz, i, i, sz, sz, u64, i, vp, sz, vp, ctypes.POINTER(SortStats)]
+        L.vxs_sort_range.restype = ctypes.c_int
         L.vxs_argsort_workspace_bytes.argtypes = [sz, i, sz, ctypes.POINTER(ctypes.c_size_t)]
         L.vxs_argsort.argtypes = [vp, sz, i, i, vp, vp, u64, i, vp, sz, vp, ctypes.POINTER(SortStats)]
         L.vxs_sort_pairs.argtypes = [vp, vp, sz, sz, i, i, u64, i, vp, sz, vp, ctypes.POINTER(SortStats)]
@@ -147,7 +149,7 @@ def lib():
 
 EXPORTED_SYMBOLS = ["vxs_sort_workspace_bytes", "vxs_sort", "vxs_sort_host", "vxs_sample",
                     "vxs_partition", "vxs_transform", "vxs_argsort_workspace_bytes", "vxs_argsort",
-                    "vxs_sort_pairs", "vxs_last_error", "vxs_key_bytes",
+                    "vxs_sort_pairs", "vxs_sort_range", "vxs_last_error", "vxs_key_bytes",
                     "vxs_base_case_capacity", "vxs_version", "vxs_profile_enable",
                     "vxs_profile_reset", "vxs_profile_read"]
 
@@ -257,14 +259,53 @@ def sort(keys, config: Optional[SortConfig] = None, key_type: Optional[str] = No
     return st
 
 
-def argsort_workspace_bytes(n: int, key_type: str, value_bytes: int = 0) -> int:
-    out = ctypes.c_size_t()
-    _check(lib().vxs_argsort_workspace_bytes(n, KEY_CODE[key_type], value_bytes, ctypes.byref(out)))
-    return out.value
+def sort_range(keys, lo: int, hi: int, config: Optional[SortConfig] = None, key_type: Optional[str] = None,
+               workspace=None, stream=None) -> SortStats:
+    """Partial sort of device keys (vxs_sort_range): afterwards
+    keys[lo:hi] is sorted and holds exactly the keys of sorted ranks lo..hi-1,
+    keys[:lo] precede them and keys[hi:] follow them (unordered)."""
+    cfg = config or SortConfig()
+    kt = infer_key_type(keys, key_type)
+    if not (_is_torch(keys) and keys.is_cuda and keys.is_contiguous()):
+        raise ValueError("sort_range takes a contiguous CUDA tensor")
+    n = _nkeys(keys, kt)
+    ws_ptr, ws_n = (None, 0) if workspace is None else (workspace.data_ptr(),
+                                                       workspace.numel() * workspace.element_size())
+    sd, has = _seed_args(cfg.seed)
+    st = SortStats()
+    _check(lib().vxs_sort_range(keys.data_ptr(), n, KEY_CODE[kt], int(cfg.order), int(lo), int(hi), sd, has,
+                                ws_ptr, ws_n, _stream_ptr(stream), ctypes.byref(st)))
+    return st
+
+
+def nth_element(keys, k: int, config: Optional[SortConfig] = None, key_type: Optional[str] = None, **kw):
+    """std::nth_element: keys[k] becomes the key of sorted rank k, smaller
+    ranks before it, larger after.  Returns the stats."""
+    return sort_range(keys, k, k + 1, config, key_type, **kw)
+
+
+def partial_sort(keys, k: int, config: Optional[SortConfig] = None, key_type: Optional[str] = None, **kw):
+    """std::partial_sort: keys[:k] becomes the k first keys in sorted order."""
+    return sort_range(keys, 0, k, config, key_type, **kw)
+
+
+def topk(keys, k: int, largest: bool = True, key_type: Optional[str] = None):
+    """The k largest (or smallest) keys, sorted from the extreme inwards, as a
+    new tensor; ``keys`` is not modified."""
+    work = keys.clone()
+    order = Order.kDescending if largest else Order.kAscending
+    partial_sort(work, k, SortConfig(order=order), key_type)
+    return work[:k].clone()
 
 
 def _seed_args(seed):
     return (0, 0) if seed is None else (int(seed) & (2**64 - 1), 1)
+
+
+def argsort_workspace_bytes(n: int, key_type: str, value_bytes: int = 0) -> int:
+    out = ctypes.c_size_t()
+    _check(lib().vxs_argsort_workspace_bytes(n, KEY_CODE[key_type], value_bytes, ctypes.byref(out)))
+    return out.value
 
 
 def argsort(keys, order: Order = Order.kAscending, key_type: Optional[str] = None, sorted_keys=None,

@@ -50,7 +50,8 @@ enum : unsigned { F_IN_B = 1u, F_RAW = 2u };
 struct SplitDesc {
   unsigned long long start, size, tile_base;
   unsigned long long aux;  // radix mode: digit multiplier M (digit = f * M >> 32)
-  unsigned flags, L;       // L: bits 0-7 fan-out exponent, bit 8 radix mode, bits 16-23 shift
+  unsigned flags, L;       // L: bits 0-7 fan-out exponent, bit 8 radix mode, bits 16-23 shift,
+                           //    bits 24-31 distinct splitter count when < 2^L - 1
 };
 
 struct Item {
@@ -178,6 +179,10 @@ struct Params {
   Item* items[kNumLists];
   unsigned long long cap_split, cap_items;
   W* out;                       // part_mode output
+  // Output positions that must end up sorted (vxs_sort_range; [0, n) for a
+  // full sort).  Children whose final range misses [rlo, rhi) are not split
+  // or sorted further -- only moved back into A (nth_element / partial_sort).
+  unsigned long long rlo, rhi;
 };
 
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
@@ -285,7 +290,7 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, unsigned lraw, Sp
   __shared__ unsigned char first[kLut + 1];
   __shared__ int s_wide;
   const int L = (int)(lraw & 0xFFu);
-  const int m = (1 << L) - 1;
+  const int m = (lraw >> 24) ? (int)(lraw >> 24) : (1 << L) - 1;  // deduplicated count, if set
   if (lraw & 0x100u) {  // radix mode: digit = (x - lo) >> shift, no table
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -583,13 +588,32 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
       Lf = 2;
       while ((1 << Lf) < Dr) ++Lf;
     }
+    unsigned meff = 0;  // distinct splitters when fewer than m (bits 24-31 of L)
     if (radix) {
       if (threadIdx.x == 0) g[0] = slo;
     } else {
-      for (int k = threadIdx.x; k < m; k += THREADS) g[k] = s[(k + 1) * step - 1];
+      // Equidistant splitters, deduplicated: low-entropy samples (few
+      // distinct values) get a short splitter list, so the lookup table has
+      // one splitter per cell and every key takes the fast path.
+      static_assert(THREADS >= 255, "one candidate per thread");
+      const int k = threadIdx.x;
+      W v = key_max<W>();
+      unsigned uq = 0;
+      if (k < m) {
+        v = s[(k + 1) * step - 1];
+        uq = (k == 0 || key_lt(s[k * step - 1], v)) ? 1u : 0u;
+      }
+      unsigned u = 0;
+      const unsigned pos = block_exclusive_scan<THREADS>(uq, &u, reinterpret_cast<unsigned*>(dcnt));
+      if (uq) g[pos] = v;
+      if (u < (unsigned)m) {
+        Lf = 1;
+        while ((1u << Lf) - 1u < u) ++Lf;
+        meff = u;
+      }
     }
     if (threadIdx.x == 0) {
-      list[p].L = (unsigned)Lf | (radix ? (0x100u | ((unsigned)dshift << 16)) : 0u);
+      list[p].L = (unsigned)Lf | (radix ? (0x100u | ((unsigned)dshift << 16)) : 0u) | (meff << 24);
       list[p].aux = dmul;
     }
     __syncthreads();
@@ -703,12 +727,29 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
     auto count_tile = [&](auto tree_tag, auto flt_tag) {
       constexpr int TREE = decltype(tree_tag)::value;
       constexpr bool FLT = decltype(flt_tag)::value;
-      if (cnt == TILE) {
+      if (cnt == TILE && TREE == 2) {  // radix: stream classify -> count
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-          const int b = classify_mode<TREE>(enc_x<FLT>(lds_key<W>(kp, i * THREADS + threadIdx.x), X), S);
-          if (b >= 0) atomicAdd(&hist[b], 1u);
-          else wide |= 1u << i;
+        for (int i = 0; i < ITEMS; ++i)
+          atomicAdd(&hist[classify_mode<TREE>(enc_x<FLT>(lds_key<W>(kp, i * THREADS + threadIdx.x), X), S)], 1u);
+      } else if (cnt == TILE) {
+        int bk[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i)
+          bk[i] = classify_mode<TREE>(enc_x<FLT>(lds_key<W>(kp, i * THREADS + threadIdx.x), X), S);
+        // a warp whose whole sub-tile is one child (low-entropy input) adds
+        // once instead of 32*ITEMS same-address atomics
+        bool same = bk[0] >= 0;
+#pragma unroll
+        for (int i = 1; i < ITEMS; ++i) same = same && bk[i] == bk[0];
+        const int b0 = __shfl_sync(0xffffffffu, bk[0], 0);
+        if (__all_sync(0xffffffffu, same && bk[0] == b0)) {
+          if ((threadIdx.x & 31) == 0) atomicAdd(&hist[b0], 32u * ITEMS);
+        } else {
+#pragma unroll
+          for (int i = 0; i < ITEMS; ++i) {
+            if (bk[i] >= 0) atomicAdd(&hist[bk[i]], 1u);
+            else wide |= 1u << i;
+          }
         }
       } else {
 #pragma unroll
@@ -824,8 +865,10 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
       __syncthreads();
       continue;
     }
+    // does child c's final range [start + off, + cnt) meet the requested output range?
+    const bool rel = d.start + off + cnt > P.rlo && d.start + off < P.rhi;
     // next-level split children
-    const bool is_split = c < nc && (c & 1) == 0 && cnt > CAP;
+    const bool is_split = c < nc && (c & 1) == 0 && cnt > CAP && rel;
     const unsigned long long my_tiles = is_split ? (unsigned long long)ntiles_dev<W>(cnt) : 0ull;
     const unsigned long long pk = is_split ? ((1ull << 40) | my_tiles) : 0ull;
     unsigned long long pk_total;
@@ -862,12 +905,12 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
     int my_list = -1;
     unsigned long long my_start = 0, my_size = 0;
     if (c < nc && !small) {
-      if (!eqc && cnt > CAP) {
+      if (!eqc && cnt > CAP && rel) {
         // split child: already queued
-      } else if (eqc && cnt > CAP) {
+      } else if (cnt > CAP) {  // equality bucket, or a child outside the requested range
         if (need_copy) my_list = kListCopyBig;
       } else {
-        my_list = (!eqc && cnt > 1) ? class_for(cnt) : (need_copy ? kListCopySmall : -1);
+        my_list = (!eqc && cnt > 1 && rel) ? class_for(cnt) : (need_copy ? kListCopySmall : -1);
       }
       my_start = d.start + off;
       my_size = cnt;
@@ -881,8 +924,9 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
           gz += s_cnt[e];
           gsort = gsort || ((e & 1) == 0 && s_cnt[e] > 1);
         }
+        const bool grel = d.start + off + gz > P.rlo && d.start + off < P.rhi;
         if (gz) {
-          my_list = gsort ? class_for(gz) : (need_copy ? kListCopySmall : -1);
+          my_list = (gsort && grel) ? class_for(gz) : (need_copy ? kListCopySmall : -1);
           my_start = d.start + off;
           my_size = gz;
         }
@@ -1366,20 +1410,41 @@ __global__ void __launch_bounds__(256) k_copy(Params<W> P) {
       for (unsigned long long i = threadIdx.x; i < item.size; i += 256) dst[i] = dec<W>(ldcs(src + i), P.xf);
     }
   }
-  // big items: every CTA takes strided chunks of every item
+  // big items: one flat space of 4096-key chunks over all items, grid-strided
+  // (each CTA walks the item list forward as its chunk index grows)
   {
     const unsigned long long nitems = P.ctrl->item_count[kListCopyBig];
     const Item* items = P.items[kListCopyBig];
     constexpr unsigned long long CH = 4096;
-    for (unsigned long long it = 0; it < nitems; ++it) {
-      const Item item = items[it];
+    unsigned long long it = 0, base = 0;
+    Item item{};
+    unsigned long long nch = 0;
+    if (nitems) {
+      item = items[0];
+      nch = (item.size + CH - 1) / CH;
+    }
+    for (unsigned long long ch = blockIdx.x; it < nitems; ch += gridDim.x) {
+      while (it < nitems && ch >= base + nch) {
+        base += nch;
+        if (++it < nitems) {
+          item = items[it];
+          nch = (item.size + CH - 1) / CH;
+        }
+      }
+      if (it >= nitems) break;
+      const unsigned long long c0 = (ch - base) * CH;
+      const unsigned long long e = c0 + CH < item.size ? c0 + CH : item.size;
       const W* src = ((item.flags & F_IN_B) ? P.b : P.a) + item.start;
       W* dst = P.a + item.start;
-      const unsigned long long nch = (item.size + CH - 1) / CH;
-      for (unsigned long long ch = blockIdx.x; ch < nch; ch += gridDim.x) {
-        const unsigned long long e = (ch + 1) * CH < item.size ? (ch + 1) * CH : item.size;
-        for (unsigned long long i = ch * CH + threadIdx.x; i < e; i += 256) dst[i] = dec<W>(ldcs(src + i), P.xf);
+      unsigned long long i = c0 + threadIdx.x;
+      for (; i + 3 * 256 < e; i += 4 * 256) {  // 4 independent loads in flight per thread
+        const W v0 = ldcs(src + i), v1 = ldcs(src + i + 256), v2 = ldcs(src + i + 512), v3 = ldcs(src + i + 768);
+        dst[i] = dec<W>(v0, P.xf);
+        dst[i + 256] = dec<W>(v1, P.xf);
+        dst[i + 512] = dec<W>(v2, P.xf);
+        dst[i + 768] = dec<W>(v3, P.xf);
       }
+      for (; i < e; i += 256) dst[i] = dec<W>(ldcs(src + i), P.xf);
     }
   }
 }

@@ -207,6 +207,8 @@ Params<W> make_params(W* keys, size_t n, int xf, uint64_t seed, unsigned char* w
   P.cap_split = L.cap_split;
   P.cap_items = L.cap_items;
   P.out = nullptr;
+  P.rlo = 0;
+  P.rhi = n;
   return P;
 }
 
@@ -332,7 +334,7 @@ vxs_status read_ctrl(const Ctrl* d_ctrl, Ctrl& h, cudaStream_t st) {
 
 template <typename W>
 vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t ws_bytes, cudaStream_t st,
-                    vxs_stats* stats) {
+                    vxs_stats* stats, size_t rlo = 0, size_t rhi = ~size_t(0)) {
   const Layout L = layout_for<W>(n);
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));
@@ -347,6 +349,8 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
     return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: provided workspace is too small");
   }
   Params<W> P = make_params<W>(keys, n, xf, seed, static_cast<unsigned char*>(ws), L);
+  P.rlo = rlo;
+  P.rhi = std::min(rhi, n);
   int launches = 0;
   {
     ProfScope ps(K_INIT, st);
@@ -1204,6 +1208,23 @@ vxs_status vxs_sort_host(void* h_keys, size_t n, vxs_key_type type, vxs_order or
   cudaStreamDestroy(st);
   if (stats) stats->kernel_launches += 0;
   return s;
+}
+
+vxs_status vxs_sort_range(void* d_keys, size_t n, vxs_key_type type, vxs_order order, size_t lo, size_t hi,
+                          uint64_t seed, int has_seed, void* d_workspace, size_t workspace_bytes, void* stream,
+                          vxs_stats* stats) {
+  if (!valid_order(order)) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: invalid order");
+  if (n > 0 && d_keys == nullptr) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: keys is NULL");
+  if (lo > hi || hi > n) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: sort_range needs lo <= hi <= n");
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  if (lo == hi) return VXS_OK;
+  const int xf = xform_for(type, order);
+  const uint64_t s = seed_for(seed, has_seed, d_keys, n);
+  return with_word(type, [&](auto* tag) {
+    using W = std::remove_pointer_t<decltype(tag)>;
+    return run_sort<W>(static_cast<W*>(d_keys), n, xf, s, d_workspace, workspace_bytes,
+                       static_cast<cudaStream_t>(stream), stats, lo, hi);
+  });
 }
 
 vxs_status vxs_argsort_workspace_bytes(size_t n, vxs_key_type type, size_t value_bytes, size_t* bytes) {

@@ -14,6 +14,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="c2-u32-asc")
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--op", default="sort", choices=["sort", "argsort", "pairs", "nth", "topk1000"])
 a = ap.parse_args()
 x, kt, desc = workloads.make(a.workload, n=a.n)
 src = torch.from_numpy(x).cuda()
@@ -21,9 +22,25 @@ buf = torch.empty_like(src)
 ws = torch.empty(vx.workspace_bytes(x.shape[0], kt), dtype=torch.uint8, device="cuda")
 cfg = vx.SortConfig(order=vx.Order(int(desc)), seed=1)
 ktarg = kt if kt in ("k128", "kv64") else None
+vals = torch.empty(x.shape[0], dtype=torch.int32, device="cuda") if a.op == "pairs" else None
+
+
+def run_op():
+    if a.op == "sort":
+        vx.sort(buf, cfg, key_type=ktarg, workspace=ws)
+    elif a.op == "argsort":
+        vx.argsort(buf, cfg.order, key_type=ktarg)
+    elif a.op == "pairs":
+        vx.sort_pairs(buf, vals, cfg, key_type=ktarg)
+    elif a.op == "nth":
+        vx.nth_element(buf, x.shape[0] // 3, cfg, key_type=ktarg, workspace=ws)
+    else:
+        vx.partial_sort(buf, 1000, cfg, key_type=ktarg, workspace=ws)
+
+
 for _ in range(2):
     buf.copy_(src)
-    vx.sort(buf, cfg, key_type=ktarg, workspace=ws)
+    run_op()
 torch.cuda.synchronize()
 vx.profile_reset()
 vx.profile_enable(True)
@@ -33,10 +50,10 @@ for _ in range(a.reps):
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    vx.sort(buf, cfg, key_type=ktarg, workspace=ws)
+    run_op()
     e.record()
     torch.cuda.synchronize()
     ev.append(s.elapsed_time(e))
 prof = vx.profile_read()
-print(a.workload, "ms/sort", round(sum(ev) / len(ev), 4),
+print(a.workload, a.op, "ms/op", round(sum(ev) / len(ev), 4),
       {k: round(v[1] / a.reps, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])})
