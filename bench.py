@@ -487,6 +487,43 @@ def run_distributed(args):
     okt = torch.tensor([1 if ok else 0], device="cuda")
     dist.all_reduce(okt, op=dist.ReduceOp.MIN)
     ms = float(t)
+    # one untimed profiled step: our kernel launches per step + dominant-kernel roofline
+    dist.barrier()
+    vx.profile_reset()
+    vx.profile_enable(True)
+    out = dist_sort(src, order=order, key_type=kt)
+    torch.cuda.synchronize()
+    prof = vx.profile_read()
+    vx.profile_enable(False)
+    launches = sum(v[0] for v in prof.values())
+    sc = [(l, m) for k, (l, m) in prof.items() if k.split("@")[0] == "k_scatter"]
+    sc_l, sc_ms = sum(l for l, _ in sc), sum(m for _, m in sc)
+    achieved = (2 * n * kb) / ((sc_ms / max(sc_l, 1)) * 1e-3) / 1e9 if sc_l else 0.0
+    ach = torch.tensor([achieved], device="cuda", dtype=torch.float64)
+    dist.all_reduce(ach, op=dist.ReduceOp.MIN)
+    # e2e through the public API at N GPUs: pinned host keys -> H2D -> dist_sort -> D2H, max over ranks
+    host = torch.empty(src.shape, dtype=src.dtype).pin_memory()
+    host.copy_(src.cpu())
+    dev_in = torch.empty_like(src)
+    host_out = torch.empty((2 * n,) + tuple(src.shape[1:]), dtype=src.dtype).pin_memory()
+    e2e_times, d2h_bytes = [], 0
+    for _ in range(min(args.steps, 5)):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dev_in.copy_(host, non_blocking=True)
+        res = dist_sort(dev_in, order=order, key_type=kt)
+        m = min(res.shape[0], host_out.shape[0])
+        host_out[:m].copy_(res[:m], non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_times.append(a.elapsed_time(b))
+        d2h_bytes = m * kb
+    te = torch.tensor([statistics.median(e2e_times)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te)
     line = None
     if rank == 0:
         line = {
@@ -501,6 +538,13 @@ def run_distributed(args):
             "gb_per_s_sorted": round(world * n * kb / (ms * 1e-3) / 1e9, 2),
             "clocks": clk.summary(),
             "peak_hbm_gbs": peak,
+            "roofline": {"bound": "hbm", "kernel": "k_scatter", "achieved": round(float(ach), 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(float(ach) / peak, 4) if peak else None, "traffic": None,
+                         "note": "min over ranks; 2*n_local*key_bytes per launch / mean launch time"},
+            "e2e": {"value": round(world * n / (e2e_ms * 1e-3) / 1e6, 2), "unit": "Mkeys/s",
+                    "h2d_bytes_per_step": n * kb, "d2h_bytes_per_step": d2h_bytes, "ms_per_step": round(e2e_ms, 3),
+                    "api": "pinned host keys per rank -> H2D -> dist_sort -> D2H (max over ranks)"},
+            "gpu_launches": int(launches) * args.steps,
         }
     dist.destroy_process_group()
     return line
@@ -518,6 +562,7 @@ def main():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-API e2e leg (ncu launch lists only)")
+    ap.add_argument("--force-dist", action="store_true", help="run the distributed path even at world size 1 (tests)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -526,7 +571,7 @@ def main():
             return
         print(json.dumps(run_reference(args)), flush=True)
         return
-    if world > 1:
+    if world > 1 or args.force_dist:
         line = run_distributed(args)
         if line is not None:
             print(json.dumps(line), flush=True)
