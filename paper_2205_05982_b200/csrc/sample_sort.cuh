@@ -1064,12 +1064,21 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     auto classify_tile = [&](auto tree_tag, auto flt_tag) {
       constexpr int TREE = decltype(tree_tag)::value;
       constexpr bool FLT = decltype(flt_tag)::value;
+      if (cnt == TILE) {  // full tile: no per-key bounds (branch-free classify)
 #pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        const int idx = i * THREADS + threadIdx.x;
-        k[i] = idx < cnt ? enc_x<FLT>(lds_key<W>(kp, idx), X) : key_max<W>();
-        bk[i] = idx < cnt ? classify_mode<TREE>(k[i], S) : -2;
-        if (bk[i] == -1) wide |= 1u << i;
+        for (int i = 0; i < ITEMS; ++i) {
+          k[i] = enc_x<FLT>(lds_key<W>(kp, i * THREADS + threadIdx.x), X);
+          bk[i] = classify_mode<TREE>(k[i], S);
+          if (bk[i] == -1) wide |= 1u << i;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const int idx = i * THREADS + threadIdx.x;
+          k[i] = idx < cnt ? enc_x<FLT>(lds_key<W>(kp, idx), X) : key_max<W>();
+          bk[i] = idx < cnt ? classify_mode<TREE>(k[i], S) : -2;
+          if (bk[i] == -1) wide |= 1u << i;
+        }
       }
     };
     if (S.use_tree == 2) {
