@@ -155,4 +155,237 @@ __device__ __forceinline__ void block_sort(W (&k)[ITEMS], W* smem) {
   }
 }
 
+// ---- counting-sort base case ------------------------------------------------
+// Keys of a final bucket are (close to) uniform over the bucket's range
+// [lo, hi]: the level above split by radix digit or by sample quantiles.  So
+// the base case is a counting sort on NB = 2*TOTAL linear bins of
+// (key - lo) >> shift, shift = bitlen(hi - lo) - log2 NB:
+//   1. block min/max, then one returning shared atomic per key (bin count and
+//      the key's rank inside its bin); sum(2*rank + 1) = sum(count^2) and
+//      max(rank) + 1 = the largest bin, both reduced over the block;
+//   2. exclusive scan of the bin counts -- thread t owns BPT consecutive
+//      counters in 16-byte groups padded so LDS.128/STS.128 are
+//      conflict-free;
+//   3. keys scattered to smem grouped by bin (padding keys fill [size, TOTAL));
+//   4. each thread takes ITEMS consecutive positions into registers and the
+//      warp runs C rounds of odd-even transposition sort, C = largest bin:
+//      pairs from different bins are already ordered and never swap, so C
+//      rounds sort every bin of <= C keys (about 1 min/max per key per round;
+//      the thread-boundary pair goes through one shuffle each way);
+//   5. bins straddling a warp boundary (<= one per boundary) are repaired by
+//      insertion sort in smem; coalesced decode + store.
+// Clustered items (sum c^2 > 4*size + 256, or a bin above 64 keys) return
+// false before touching the output; the caller sorts them with the network.
+// Equal keys are bitwise identical in the transformed domain, so the order
+// among them is immaterial.
+template <typename W, int THREADS, int ITEMS>
+struct BinSort {
+  static constexpr int kTotal = THREADS * ITEMS;
+  static constexpr int kNB = kTotal <= 4096 ? 2 * kTotal : kTotal;
+  static constexpr int kBPT = kNB / THREADS;  // bins per thread in the scan
+  static constexpr int kNBBits = kNB == 512 ? 9 : kNB == 1024 ? 10 : kNB == 2048 ? 11 : kNB == 4096 ? 12 : kNB == 8192 ? 13 : 14;
+  static constexpr int kEnd = kNB + kNB / 8;  // padded slot of bin NB (end sentinel)
+  static constexpr int kDummy = kEnd + 1;     // slot of bin NB + 1 (padding keys)
+  static constexpr int kCnt = (kDummy + 4) & ~3;
+  static constexpr int kMaxBin = 64;
+  static constexpr size_t kSmem = (size_t)kTotal * sizeof(W) + (size_t)kCnt * 4;
+  static_assert((1 << kNBBits) == kNB && kBPT % 4 == 0 && kBPT <= 32, "bin count");
+  // 4 pad words after every 32 counters: thread t's group starts at bank 4t
+  __host__ __device__ static __forceinline__ int slot(int b) { return b + ((b >> 3) & ~3); }
+  // smem position of key p: the 16-byte chunks of row r = p / ITEMS are
+  // XOR-swizzled by r & 7 so the per-thread row loads/stores (LDS.128 /
+  // STS.128, rows 64-256 B apart) are conflict-free.  Each chunk bit is
+  // XORed with a strictly higher bit, so this is a bijection.
+  static constexpr int kLogItems = ITEMS == 4 ? 2 : ITEMS == 8 ? 3 : ITEMS == 16 ? 4 : 5;
+  static constexpr int kLogKpc = sizeof(W) == 2 ? 3 : sizeof(W) == 4 ? 2 : sizeof(W) == 8 ? 1 : 0;
+  __device__ static __forceinline__ int swz(int p) { return p ^ (((p >> kLogItems) & 7) << kLogKpc); }
+};
+
+template <typename W, int THREADS, int ITEMS>
+__device__ __forceinline__ void block_minmax(const W (&k)[ITEMS], int size, W& lo, W& hi, W* red_lo, W* red_hi) {
+  constexpr int NW = THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  lo = k[0];
+  hi = k[0];
+#pragma unroll
+  for (int i = 1; i < ITEMS; ++i) {
+    if (i * THREADS + (int)threadIdx.x < size) {
+      if (key_lt(k[i], lo)) lo = k[i];
+      if (key_lt(hi, k[i])) hi = k[i];
+    }
+  }
+  const bool has = (int)threadIdx.x < size;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const W a = shfl_xor(lo, o), b = shfl_xor(hi, o);
+    const bool oh = __shfl_xor_sync(0xffffffffu, has ? 1 : 0, o) != 0;
+    if (oh && key_lt(a, lo)) lo = a;
+    if (oh && key_lt(hi, b)) hi = b;
+  }
+  if (lane == 0) {
+    red_lo[warp] = lo;
+    red_hi[warp] = hi;
+  }
+  __syncthreads();
+  lo = red_lo[0];
+  hi = red_hi[0];
+  const int nwv = (size + 31) / 32 < NW ? (size + 31) / 32 : NW;
+  for (int w = 1; w < nwv; ++w) {
+    if (key_lt(red_lo[w], lo)) lo = red_lo[w];
+    if (key_lt(hi, red_hi[w])) hi = red_hi[w];
+  }
+}
+
+// k[]: keys striped (key i*THREADS + tid), transformed domain, padded with
+// key_max beyond `size`.  Writes the sorted, decoded item to dst and returns
+// true, or returns false (nothing written, k[] untouched) when the bins are
+// too unbalanced.  smem: BinSort<W,THREADS,ITEMS>::kSmem bytes.
+template <typename W, int THREADS, int ITEMS, bool FLT>
+__device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, unsigned char* smem, W* dst,
+                                              const Xf<W>& X) {
+  using BS = BinSort<W, THREADS, ITEMS>;
+  constexpr int TOTAL = BS::kTotal;
+  constexpr int NB = BS::kNB;
+  constexpr int BPT = BS::kBPT;
+  constexpr int NW = THREADS / 32;
+  constexpr int NV = ITEMS * (int)sizeof(W) / 16;  // uint4 per thread row
+  static_assert(NV * 16 == ITEMS * (int)sizeof(W), "vector rows");
+  W* sk = reinterpret_cast<W*>(smem);  // keys grouped by bin, then sorted
+  unsigned* cnt = reinterpret_cast<unsigned*>(sk + TOTAL);
+  __shared__ W red_lo[NW];
+  __shared__ W red_hi[NW];
+  __shared__ unsigned s_tot[NW];
+  __shared__ unsigned s_sq[NW];
+  __shared__ unsigned s_mx[NW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int j = tid; j < BS::kCnt / 4; j += THREADS) reinterpret_cast<uint4*>(cnt)[j] = make_uint4(0, 0, 0, 0);
+  W lo, hi;
+  block_minmax<W, THREADS, ITEMS>(k, size, lo, hi, red_lo, red_hi);  // (its barrier covers cnt)
+  const int bl = key_bitlen(key_sub(hi, lo));
+  const int shift = bl > BS::kNBBits ? bl - BS::kNBBits : 0;
+  unsigned br[ITEMS];  // bin << 16 | rank inside the bin
+  unsigned sq = 0;     // sum over keys of 2*rank + 1 = sum over bins of count^2
+  unsigned mx = 0;     // largest rank
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const bool valid = i * THREADS + tid < size;
+    const unsigned b = valid ? key_shr32(key_sub(k[i], lo), shift) : (unsigned)(NB + 1);
+    const unsigned r = atomicAdd(&cnt[BS::slot((int)b)], 1u);
+    br[i] = (b << 16) | r;
+    sq += valid ? 2u * r + 1u : 0u;
+    mx = valid ? umax(mx, r) : mx;
+  }
+  __syncthreads();
+  // exclusive scan over the bins; thread t owns bins [t*BPT, (t+1)*BPT)
+  uint4* cg = reinterpret_cast<uint4*>(cnt + BS::slot(tid * BPT));
+  unsigned sum = 0;
+#pragma unroll
+  for (int j = 0; j < BPT / 4; ++j) {
+    const uint4 c = cg[j];
+    sum += c.x + c.y + c.z + c.w;
+  }
+  unsigned incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    mx = umax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (lane == 31) s_tot[warp] = incl;
+  if (lane == 0) {
+    s_sq[warp] = sq;
+    s_mx[warp] = mx;
+  }
+  __syncthreads();
+  unsigned base = incl - sum, tsq = 0, rounds = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    base += w < warp ? s_tot[w] : 0u;
+    tsq += s_sq[w];
+    rounds = umax(rounds, s_mx[w]);
+  }
+  rounds += 1;  // largest bin
+  // block-uniform rejection; cnt is no longer read
+  if (tsq > 4u * (unsigned)size + 256u || rounds > (unsigned)BS::kMaxBin) return false;
+#pragma unroll
+  for (int j = 0; j < BPT / 4; ++j) {  // (only this thread touches these counters)
+    uint4 c = cg[j];
+    const unsigned x = base, y = x + c.x, z = y + c.y, w = z + c.z;
+    base = w + c.w;
+    cg[j] = make_uint4(x, y, z, w);
+  }
+  if (tid == THREADS - 1) {
+    cnt[BS::kEnd] = (unsigned)size;
+    cnt[BS::kDummy] = (unsigned)size;  // padding keys go to [size, TOTAL)
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) sk[BS::swz((int)(cnt[BS::slot((int)(br[i] >> 16))] + (br[i] & 0xFFFFu)))] = k[i];
+  __syncthreads();
+  // odd-even transposition rounds over this thread's row of ITEMS positions
+  W v[ITEMS];
+  {
+    const uint4* row = reinterpret_cast<const uint4*>(sk);
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      const uint4 t = row[(tid * NV + q) ^ (tid & 7)];
+      memcpy(reinterpret_cast<char*>(v) + 16 * q, &t, 16);
+    }
+  }
+  if (rounds > 1) {
+#pragma unroll 1
+    for (unsigned r = 0; r < rounds; r += 2) {
+#pragma unroll
+      for (int i = 0; i + 1 < ITEMS; i += 2) cas(v[i], v[i + 1]);
+#pragma unroll
+      for (int i = 1; i + 1 < ITEMS; i += 2) cas(v[i], v[i + 1]);
+      const W nx = shfl_next(v[0]);
+      const W pv = shfl_prev(v[ITEMS - 1]);
+      if (lane < 31 && key_lt(nx, v[ITEMS - 1])) v[ITEMS - 1] = nx;
+      if (lane > 0 && key_lt(v[0], pv)) v[0] = pv;
+    }
+  }
+  {
+    uint4* row = reinterpret_cast<uint4*>(sk);
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      uint4 t;
+      memcpy(&t, reinterpret_cast<const char*>(v) + 16 * q, 16);
+      row[(tid * NV + q) ^ (tid & 7)] = t;
+    }
+  }
+  __syncthreads();
+  if (NW > 1 && rounds > 1 && lane == 0 && warp > 0) {  // bin straddling the boundary before this warp
+    const int p = warp * 32 * ITEMS;
+    if (p < size) {
+      const int b = (int)key_shr32(key_sub(sk[BS::swz(p)], lo), shift);
+      const int s = (int)cnt[BS::slot(b)], e = (int)cnt[BS::slot(b + 1)];
+      if (s < p) {
+        for (int a = s + 1; a < e; ++a) {
+          const W x = sk[BS::swz(a)];
+          int q = a;
+          while (q > s && key_lt(x, sk[BS::swz(q - 1)])) {
+            sk[BS::swz(q)] = sk[BS::swz(q - 1)];
+            --q;
+          }
+          sk[BS::swz(q)] = x;
+        }
+      }
+    }
+    __syncwarp(1u);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int idx = i * THREADS + tid;
+    if (idx < size) dst[idx] = dec_x<FLT>(sk[BS::swz(idx)], X);
+  }
+  __syncthreads();
+  return true;
+}
+
 }  // namespace vxs

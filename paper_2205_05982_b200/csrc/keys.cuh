@@ -368,5 +368,18 @@ template <>
 __device__ __forceinline__ U128 shfl_xor<U128>(U128 v, int m) {
   return U128{__shfl_xor_sync(0xffffffffu, v.lo, m), __shfl_xor_sync(0xffffffffu, v.hi, m)};
 }
+// Value of lane + 1 (shfl_next) / lane - 1 (shfl_prev); the edge lanes get their own.
+template <typename W>
+__device__ __forceinline__ W shfl_next(W v) {
+  if constexpr (sizeof(W) == 16) return W{__shfl_down_sync(0xffffffffu, v.lo, 1), __shfl_down_sync(0xffffffffu, v.hi, 1)};
+  else if constexpr (sizeof(W) == 2) return (W)__shfl_down_sync(0xffffffffu, (unsigned)v, 1);
+  else return __shfl_down_sync(0xffffffffu, v, 1);
+}
+template <typename W>
+__device__ __forceinline__ W shfl_prev(W v) {
+  if constexpr (sizeof(W) == 16) return W{__shfl_up_sync(0xffffffffu, v.lo, 1), __shfl_up_sync(0xffffffffu, v.hi, 1)};
+  else if constexpr (sizeof(W) == 2) return (W)__shfl_up_sync(0xffffffffu, (unsigned)v, 1);
+  else return __shfl_up_sync(0xffffffffu, v, 1);
+}
 
 }  // namespace vxs

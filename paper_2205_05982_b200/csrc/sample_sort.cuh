@@ -40,7 +40,7 @@ constexpr int kChildStride = 512;   // child slots per split bucket (2*(2^L-1)+2
 constexpr int kNumSortClasses = 5;  // base-case size classes
 constexpr int kListCopySmall = kNumSortClasses;
 constexpr int kListCopyBig = kNumSortClasses + 1;
-constexpr int kListFallback = kNumSortClasses + 2;  // >= 8-byte items the prefix sort rejected
+constexpr int kListFallback = kNumSortClasses + 2;  // items the counting sort rejected
 constexpr int kNumLists = kNumSortClasses + 3;
 constexpr int kMaxSamples = 4096;
 constexpr unsigned long long kTileMask = (1ull << 40) - 1;
@@ -1199,125 +1199,20 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   }
 }
 
-// Prefix-compressed base case for 64/128-bit keys: sort 32-bit words
-// (top PB varying bits of key - min) << IB | index with the u32 warp network
-// (a 64-bit compare-exchange costs ~3x a 32-bit one), then repair runs of
-// equal prefixes by full-key insertion sort and gather the keys.  Items whose
-// prefixes collide in long runs (clustered keys) use the full-width sort.
-template <typename W, int THREADS, int ITEMS>
-__device__ __forceinline__ bool prefix_sort_item(W (&k)[ITEMS], int size, unsigned char* smem, W* dst, const Xf<W>& X) {
-  constexpr int TOTAL = THREADS * ITEMS;
-  constexpr int IB = (TOTAL <= 1024) ? 10 : (TOTAL <= 2048 ? 11 : (TOTAL <= 4096 ? 12 : 13));
-  constexpr int PB = 32 - IB;
-  constexpr int NW = THREADS / 32;
-  constexpr int kMaxRun = 32;
-  W* sk = reinterpret_cast<W*>(smem);                                   // keys by load index
-  unsigned* sw = reinterpret_cast<unsigned*>(sk + TOTAL);               // padded words
-  __shared__ W red_lo[NW];
-  __shared__ W red_hi[NW];
-  __shared__ int s_bad;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // min / max over valid keys (valid keys are a prefix of the striped order)
-  W lo = k[0], hi = k[0];
-#pragma unroll
-  for (int i = 1; i < ITEMS; ++i) {
-    if (i * THREADS + (int)threadIdx.x < size) {
-      if (key_lt(k[i], lo)) lo = k[i];
-      if (key_lt(hi, k[i])) hi = k[i];
-    }
-  }
-  const bool has = (int)threadIdx.x < size;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const W a = shfl_xor(lo, o), b = shfl_xor(hi, o);
-    const bool oh = __shfl_xor_sync(0xffffffffu, has ? 1 : 0, o) != 0;
-    if (oh && key_lt(a, lo)) lo = a;
-    if (oh && key_lt(hi, b)) hi = b;
-  }
-  if (lane == 0) {
-    red_lo[warp] = lo;
-    red_hi[warp] = hi;
-  }
-  if (threadIdx.x == 0) s_bad = 0;
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) sk[i * THREADS + threadIdx.x] = k[i];
-  __syncthreads();
-  lo = red_lo[0];
-  hi = red_hi[0];
-  const int nwv = (size + 31) / 32 < NW ? (size + 31) / 32 : NW;
-  for (int w = 1; w < nwv; ++w) {
-    if (key_lt(red_lo[w], lo)) lo = red_lo[w];
-    if (key_lt(hi, red_hi[w])) hi = red_hi[w];
-  }
-  const int bl = key_bitlen(key_sub(hi, lo));
-  const int shift = bl > PB ? bl - PB : 0;
-  unsigned wv[ITEMS];
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int idx = i * THREADS + threadIdx.x;
-    wv[i] = idx < size ? ((key_shr32(key_sub(k[i], lo), shift) << IB) | (unsigned)idx) : 0xFFFFFFFFu;
-  }
-  block_sort<unsigned, THREADS, ITEMS, true>(wv, sw);
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) sw[pad_idx<unsigned>(threadIdx.x * ITEMS + i)] = wv[i];
-  __syncthreads();
-  // repair runs of equal prefixes (only when the prefix dropped bits and some
-  // neighbouring words share a prefix: checked in registers, one block vote)
-  bool dup = false;
-#pragma unroll
-  for (int i = 0; i + 1 < ITEMS; ++i) dup = dup || ((wv[i] >> IB) == (wv[i + 1] >> IB) && wv[i + 1] != 0xFFFFFFFFu);
-  {
-    const int nxt = threadIdx.x * ITEMS + ITEMS;
-    if (nxt < size) dup = dup || ((wv[ITEMS - 1] >> IB) == (sw[pad_idx<unsigned>(nxt)] >> IB));
-  }
-  if (shift > 0 && __syncthreads_or(dup ? 1 : 0)) {
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const int pos = threadIdx.x * ITEMS + i;
-      if (pos + 1 < size) {
-        const unsigned w0 = wv[i];
-        const unsigned wprev = pos > 0 ? sw[pad_idx<unsigned>(pos - 1)] : 0xFFFFFFFFu;
-        const unsigned wnext = sw[pad_idx<unsigned>(pos + 1)];
-        const bool start = (w0 >> IB) == (wnext >> IB) && (pos == 0 || (wprev >> IB) != (w0 >> IB));
-        if (start) {
-          int e = pos + 1;
-          while (e < size && (sw[pad_idx<unsigned>(e)] >> IB) == (w0 >> IB)) ++e;
-          if (e - pos > kMaxRun) {
-            s_bad = 1;
-          } else {
-            for (int a = pos + 1; a < e; ++a) {
-              const unsigned v = sw[pad_idx<unsigned>(a)];
-              const W kv = sk[v & ((1u << IB) - 1)];
-              int j = a;
-              while (j > pos && key_lt(kv, sk[sw[pad_idx<unsigned>(j - 1)] & ((1u << IB) - 1)])) {
-                sw[pad_idx<unsigned>(j)] = sw[pad_idx<unsigned>(j - 1)];
-                --j;
-              }
-              sw[pad_idx<unsigned>(j)] = v;
-            }
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (s_bad) return false;
-  }
-  if (X.flt) {
-    for (int idx = threadIdx.x; idx < size; idx += THREADS)
-      dst[idx] = dec_x<true>(sk[sw[pad_idx<unsigned>(idx)] & ((1u << IB) - 1)], X);
-  } else {
-    for (int idx = threadIdx.x; idx < size; idx += THREADS)
-      dst[idx] = dec_x<false>(sk[sw[pad_idx<unsigned>(idx)] & ((1u << IB) - 1)], X);
-  }
-  __syncthreads();
-  return true;
+// Register budget of the counting-sort classes: 64 (<= 4-byte keys), 80
+// (8-byte) or 128 (16-byte) registers per thread, so several CTAs share an SM
+// and hide each other's item loads.
+template <typename W, int CLS>
+constexpr int final_min_blocks() {
+  return CLS == 0 ? 1 : (sizeof(W) <= 4 ? 1024 : sizeof(W) == 8 ? 768 : 512) / SortClass<CLS>::T;
 }
 
-// Base case over one size class: load <= T*I keys, pad with the transformed
-// maximum, block_sort (or the prefix-compressed sort for >= 8-byte keys),
-// decode, write back into A.
+// Base case over one size class: load <= T*I keys (pad: transformed maximum),
+// sort them -- class 0 (<= 256 keys) with the warp bitonic network, larger
+// classes with the counting sort (block_sort.cuh bin_sort_item) -- decode,
+// write back into A.
 template <typename W, int CLS>
-__global__ void __launch_bounds__(SortClass<CLS>::T) k_final(Params<W> P) {
+__global__ void __launch_bounds__(SortClass<CLS>::T, final_min_blocks<W, CLS>()) k_final(Params<W> P) {
   constexpr int THREADS = SortClass<CLS>::T;
   constexpr int ITEMS = SortClass<CLS>::I;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1344,20 +1239,19 @@ __global__ void __launch_bounds__(SortClass<CLS>::T) k_final(Params<W> P) {
       }
     }
     W* dst = P.a + item.start;
-    if constexpr (sizeof(W) >= 8 && THREADS * ITEMS >= 512) {
-      // keys of 8+ bytes: prefix-compressed sort; rejected items (clustered
-      // keys) go to the full-width fallback kernel, keeping this one lean
-      if (!prefix_sort_item<W, THREADS, ITEMS>(k, size, smem_raw, dst, X) && threadIdx.x == 0) {
+    if constexpr (CLS >= 1) {
+      // counting-sort base case; items it rejects (clustered keys, decided
+      // block-uniformly) go to the full-width network fallback kernel
+      const bool done = X.flt ? bin_sort_item<W, THREADS, ITEMS, true>(k, size, smem_raw, dst, X)
+                              : bin_sort_item<W, THREADS, ITEMS, false>(k, size, smem_raw, dst, X);
+      if (!done && threadIdx.x == 0) {
         const unsigned long long slot = atomicAdd(&P.ctrl->item_count[kListFallback], 1ull);
         if (slot < P.cap_items) P.items[kListFallback][slot] = item;
         else P.ctrl->error = 3;
       }
-      __syncthreads();
     } else {
-      // 32-bit and narrower keys merge inside the warp with __shfl_xor_sync
-      // networks (measured faster); 64/128-bit keys use shared-memory merge path.
-      constexpr bool kWN = SortClass<CLS>::kWarpNet || sizeof(W) <= 4;
-      block_sort<W, THREADS, ITEMS, kWN>(k, sm);
+      // smallest class: bitonic network merged inside the warp (__shfl_xor_sync)
+      block_sort<W, THREADS, ITEMS, true>(k, sm);
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) sm[pad_idx<W>(threadIdx.x * ITEMS + i)] = k[i];
       __syncthreads();
@@ -1371,7 +1265,7 @@ __global__ void __launch_bounds__(SortClass<CLS>::T) k_final(Params<W> P) {
   }
 }
 
-// Full-width merge sort of the items the prefix-compressed sort rejected
+// Full-width bitonic/merge-path sort of the items the counting sort rejected
 // (persistent; reads the fallback count on the device, usually zero).
 template <typename W>
 __global__ void __launch_bounds__(SortClass<4>::T) k_final_fallback(Params<W> P) {

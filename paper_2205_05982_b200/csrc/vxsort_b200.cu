@@ -277,9 +277,7 @@ template <typename W, int CLS>
 void launch_final(Params<W>& P, unsigned long long count, cudaStream_t st) {
   constexpr int T = SortClass<CLS>::T;
   constexpr int TOT = T * SortClass<CLS>::I;
-  constexpr size_t smem_a = (size_t)padded_size<W>(TOT) * sizeof(W);
-  constexpr size_t smem_b = (size_t)TOT * sizeof(W) + (size_t)padded_size<unsigned>(TOT) * sizeof(unsigned);
-  constexpr size_t smem = smem_a > smem_b ? smem_a : smem_b;
+  constexpr size_t smem = CLS >= 1 ? BinSort<W, T, SortClass<CLS>::I>::kSmem : (size_t)padded_size<W>(TOT) * sizeof(W);
   ProfScope ps(K_FINAL0 + CLS, st);
   auto fn = k_final<W, CLS>;
   int g = grid_for((const void*)fn, T, smem);
@@ -400,9 +398,9 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
   if constexpr (Cfg<W>::kCap >= 8192) {
     if (h.item_count[4]) { launch_final<W, 4>(P, h.item_count[4], st); ++launches; }
   }
-  if constexpr (sizeof(W) >= 8) {
-    // items rejected by the prefix-compressed base case (count lives on the device)
-    if (h.item_count[0] + h.item_count[1] + h.item_count[2] + h.item_count[3] + h.item_count[4]) {
+  {
+    // items rejected by the counting-sort base case (count lives on the device)
+    if (h.item_count[1] + h.item_count[2] + h.item_count[3] + h.item_count[4]) {
       ProfScope ps(K_FALLBACK, st);
       constexpr int ITEMS = sizeof(W) >= 16 ? 8 : 16;
       constexpr size_t smem = (size_t)padded_size<W>(SortClass<4>::T * ITEMS) * sizeof(W);
