@@ -255,6 +255,28 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* total, T* scratch /*[3
 constexpr int kLutBits = 12;
 constexpr int kLut = 1 << kLutBits;
 
+// Radix-mode digit of x: f = (max(x, lo) - lo) >> shift (top ~24 varying
+// bits of the bucket's sample range, saturated to 32 bits for keys far above
+// it), digit = min(umulhi(f, mul), m).  Monotone in x, so child ids ascend
+// with the keys; a single IMAD.HI per key instead of a 64-bit product.
+__device__ __forceinline__ unsigned radix_digit(uint16_t x, uint16_t lo, int shift, unsigned mul, unsigned m) {
+  const unsigned xl = x > lo ? x : lo;
+  return umin(__umulhi((xl - lo) >> shift, mul), m);
+}
+__device__ __forceinline__ unsigned radix_digit(uint32_t x, uint32_t lo, int shift, unsigned mul, unsigned m) {
+  const unsigned xl = umax(x, lo);
+  return umin(__umulhi((xl - lo) >> shift, mul), m);
+}
+__device__ __forceinline__ unsigned radix_digit(unsigned long long x, unsigned long long lo, int shift, unsigned mul,
+                                                unsigned m) {
+  const unsigned long long f = ((x > lo ? x : lo) - lo) >> shift;
+  return umin(__umulhi((f >> 32) ? 0xFFFFFFFFu : (unsigned)f, mul), m);
+}
+__device__ __forceinline__ unsigned radix_digit(const U128& x, const U128& lo, int shift, unsigned mul, unsigned m) {
+  if (key_lt(x, lo)) return 0u;
+  return umin(__umulhi(key_shr32(key_sub(x, lo), shift), mul), m);
+}
+
 template <typename W>
 struct SplSmem {
   W srt[257];   // m splitters, padded with the maximum up to 255, + sentinel
@@ -262,7 +284,7 @@ struct SplSmem {
   W lo;
   unsigned cmax;
   int shift, m, use_tree;  // use_tree: 0 table, 1 tree, 2 radix (equal-width digits)
-  unsigned long long mul;  // radix mode multiplier
+  unsigned mul;  // radix mode multiplier (radix_digit)
   unsigned short lut[kLut];  // (first, end) splitter index of cell c, packed lo | hi << 8
 };
 
@@ -297,7 +319,7 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, unsigned lraw, Sp
       S.lo = g_srt[0];
       S.shift = (int)((lraw >> 16) & 0xFFu);
       S.m = m;
-      S.mul = aux;
+      S.mul = (unsigned)aux;
       S.use_tree = 2;
     }
     __syncthreads();
@@ -360,11 +382,7 @@ __device__ __forceinline__ int classify_mode(const W& x, const SplSmem<W>& S) {
   if constexpr (MODE == 2) {
     // equal-width digits over the sample range (the sample certified them
     // balanced); keys below/above the range clamp to the first/last digit
-    const unsigned f = key_shr32(key_sub(x, S.lo), S.shift);
-    unsigned dgt = (unsigned)__umul64hi((unsigned long long)f << 32, S.mul);
-    dgt = dgt < (unsigned)S.m ? dgt : (unsigned)S.m;
-    dgt = key_lt(x, S.lo) ? 0u : dgt;
-    return 2 * (int)dgt;
+    return 2 * (int)radix_digit(x, S.lo, S.shift, S.mul, (unsigned)S.m);
   } else if constexpr (MODE == 1) {
     int j = 1;
 #pragma unroll
@@ -397,15 +415,9 @@ struct RadixReg {
   W lo;
   int shift;
   unsigned m;
-  unsigned long long mul;
+  unsigned mul;
   __device__ __forceinline__ explicit RadixReg(const SplSmem<W>& S) : lo(S.lo), shift(S.shift), m((unsigned)S.m), mul(S.mul) {}
-  __device__ __forceinline__ int child(const W& x) const {
-    const unsigned f = key_shr32(key_sub(x, lo), shift);
-    unsigned dgt = (unsigned)__umul64hi((unsigned long long)f << 32, mul);
-    dgt = dgt < m ? dgt : m;
-    dgt = key_lt(x, lo) ? 0u : dgt;
-    return 2 * (int)dgt;
-  }
+  __device__ __forceinline__ int child(const W& x) const { return 2 * (int)radix_digit(x, lo, shift, mul, m); }
 };
 
 template <typename W>
@@ -538,19 +550,17 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
     const W slo = s[0];
     const W srange = key_sub(s[S - 1], slo);
     const int bl = key_bitlen(srange);
-    const int dshift = bl > 32 ? bl - 32 : 0;  // f = top 32 bits of (x - lo)
+    const int dshift = bl > 24 ? bl - 24 : 0;  // f = top 24 bits of (x - lo)
     const unsigned long long rf = key_shr32(srange, dshift);
     auto certify = [&](int D, unsigned long long& mul) -> bool {
       const int mr = D - 1;
       mul = ((unsigned long long)D << 32) / (rf + 1);
+      if (mul > 0xFFFFFFFFull) mul = 0xFFFFFFFFull;  // fewer code values than digits
       for (int k = threadIdx.x; k <= mr; k += THREADS) dcnt[k] = 0;
       if (threadIdx.x == 0) s_maxc = 0;
       __syncthreads();
-      for (int i = threadIdx.x; i < S; i += THREADS) {
-        const unsigned f = key_shr32(key_sub(s[i], slo), dshift);
-        const unsigned dg = (unsigned)__umul64hi((unsigned long long)f << 32, mul);
-        atomicAdd(&dcnt[dg < (unsigned)mr ? dg : (unsigned)mr], 1u);
-      }
+      for (int i = threadIdx.x; i < S; i += THREADS)
+        atomicAdd(&dcnt[radix_digit(s[i], slo, dshift, (unsigned)mul, (unsigned)mr)], 1u);
       __syncthreads();
       unsigned used = 0;
       for (int k = threadIdx.x; k <= mr; k += THREADS) {
