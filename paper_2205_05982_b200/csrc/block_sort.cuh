@@ -201,26 +201,32 @@ struct BinSort {
   __device__ static __forceinline__ int swz(int p) { return p ^ (((p >> kLogItems) & 7) << kLogKpc); }
 };
 
+// Block min / max of k[] over all THREADS*ITEMS slots (the caller pads with
+// a copy of a real key, so no per-slot validity test is needed).
+template <typename W>
+__device__ __forceinline__ W key_min2(const W& a, const W& b) { return key_lt(b, a) ? b : a; }
+template <typename W>
+__device__ __forceinline__ W key_max2(const W& a, const W& b) { return key_lt(a, b) ? b : a; }
+template <>
+__device__ __forceinline__ uint32_t key_min2<uint32_t>(const uint32_t& a, const uint32_t& b) { return umin(a, b); }
+template <>
+__device__ __forceinline__ uint32_t key_max2<uint32_t>(const uint32_t& a, const uint32_t& b) { return umax(a, b); }
+
 template <typename W, int THREADS, int ITEMS>
-__device__ __forceinline__ void block_minmax(const W (&k)[ITEMS], int size, W& lo, W& hi, W* red_lo, W* red_hi) {
+__device__ __forceinline__ void block_minmax(const W (&k)[ITEMS], W& lo, W& hi, W* red_lo, W* red_hi) {
   constexpr int NW = THREADS / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   lo = k[0];
   hi = k[0];
 #pragma unroll
   for (int i = 1; i < ITEMS; ++i) {
-    if (i * THREADS + (int)threadIdx.x < size) {
-      if (key_lt(k[i], lo)) lo = k[i];
-      if (key_lt(hi, k[i])) hi = k[i];
-    }
+    lo = key_min2(lo, k[i]);
+    hi = key_max2(hi, k[i]);
   }
-  const bool has = (int)threadIdx.x < size;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    const W a = shfl_xor(lo, o), b = shfl_xor(hi, o);
-    const bool oh = __shfl_xor_sync(0xffffffffu, has ? 1 : 0, o) != 0;
-    if (oh && key_lt(a, lo)) lo = a;
-    if (oh && key_lt(hi, b)) hi = b;
+    lo = key_min2(lo, shfl_xor(lo, o));
+    hi = key_max2(hi, shfl_xor(hi, o));
   }
   if (lane == 0) {
     red_lo[warp] = lo;
@@ -229,15 +235,15 @@ __device__ __forceinline__ void block_minmax(const W (&k)[ITEMS], int size, W& l
   __syncthreads();
   lo = red_lo[0];
   hi = red_hi[0];
-  const int nwv = (size + 31) / 32 < NW ? (size + 31) / 32 : NW;
-  for (int w = 1; w < nwv; ++w) {
-    if (key_lt(red_lo[w], lo)) lo = red_lo[w];
-    if (key_lt(hi, red_hi[w])) hi = red_hi[w];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) {
+    lo = key_min2(lo, red_lo[w]);
+    hi = key_max2(hi, red_hi[w]);
   }
 }
 
-// k[]: keys striped (key i*THREADS + tid), transformed domain, padded with
-// key_max beyond `size`.  Writes the sorted, decoded item to dst and returns
+// k[]: keys striped (key i*THREADS + tid), transformed domain, padded
+// beyond `size` with a copy of one of the item's keys (neutral for min/max).  Writes the sorted, decoded item to dst and returns
 // true, or returns false (nothing written, k[] untouched) when the bins are
 // too unbalanced.  smem: BinSort<W,THREADS,ITEMS>::kSmem bytes.
 template <typename W, int THREADS, int ITEMS, bool FLT>
@@ -250,7 +256,11 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
   constexpr int NW = THREADS / 32;
   constexpr int NV = ITEMS * (int)sizeof(W) / 16;  // uint4 per thread row
   static_assert(NV * 16 == ITEMS * (int)sizeof(W), "vector rows");
-  W* sk = reinterpret_cast<W*>(smem);  // keys grouped by bin, then sorted
+  // (the dynamic smem is named here, not through the generic `smem`
+  // pointer, so every access is a plain LDS/STS off a shared-window symbol)
+  (void)smem;
+  extern __shared__ __align__(128) unsigned char bs_dyn[];
+  W* sk = reinterpret_cast<W*>(bs_dyn);  // keys grouped by bin, then sorted
   unsigned* cnt = reinterpret_cast<unsigned*>(sk + TOTAL);
   __shared__ W red_lo[NW];
   __shared__ W red_hi[NW];
@@ -260,19 +270,19 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int j = tid; j < BS::kCnt / 4; j += THREADS) reinterpret_cast<uint4*>(cnt)[j] = make_uint4(0, 0, 0, 0);
   W lo, hi;
-  block_minmax<W, THREADS, ITEMS>(k, size, lo, hi, red_lo, red_hi);  // (its barrier covers cnt)
+  block_minmax<W, THREADS, ITEMS>(k, lo, hi, red_lo, red_hi);  // (its barrier covers cnt)
   const int bl = key_bitlen(key_sub(hi, lo));
   const int shift = bl > BS::kNBBits ? bl - BS::kNBBits : 0;
-  unsigned br[ITEMS];  // bin << 16 | rank inside the bin
+  unsigned br[ITEMS];  // padded counter slot << 16 | rank inside the bin
   unsigned sq = 0;     // sum over keys of 2*rank + 1 = sum over bins of count^2
   unsigned mx = 0;     // largest rank
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const bool valid = i * THREADS + tid < size;
-    const unsigned b = valid ? key_shr32(key_sub(k[i], lo), shift) : (unsigned)(NB + 1);
-    const unsigned r = atomicAdd(&cnt[BS::slot((int)b)], 1u);
-    br[i] = (b << 16) | r;
-    sq += valid ? 2u * r + 1u : 0u;
+    const int sl = valid ? BS::slot((int)key_shr32(key_sub(k[i], lo), shift)) : BS::kDummy;
+    const unsigned r = atomicAdd(&cnt[sl], 1u);
+    br[i] = ((unsigned)sl << 16) | r;
+    sq += 2u * r + 1u;
     mx = valid ? umax(mx, r) : mx;
   }
   __syncthreads();
@@ -310,7 +320,8 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
   }
   rounds += 1;  // largest bin
   // block-uniform rejection; cnt is no longer read
-  if (tsq > 4u * (unsigned)size + 256u || rounds > (unsigned)BS::kMaxBin) return false;
+  const unsigned pad = (unsigned)(TOTAL - size);  // the dummy bin adds pad^2
+  if (tsq - pad * pad > 4u * (unsigned)size + 256u || rounds > (unsigned)BS::kMaxBin) return false;
 #pragma unroll
   for (int j = 0; j < BPT / 4; ++j) {  // (only this thread touches these counters)
     uint4 c = cg[j];
@@ -324,7 +335,8 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
   }
   __syncthreads();
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) sk[BS::swz((int)(cnt[BS::slot((int)(br[i] >> 16))] + (br[i] & 0xFFFFu)))] = k[i];
+  for (int i = 0; i < ITEMS; ++i)
+    sk[BS::swz((int)(cnt[br[i] >> 16] + (br[i] & 0xFFFFu)))] = i * THREADS + tid < size ? k[i] : key_max<W>();
   __syncthreads();
   // odd-even transposition rounds over this thread's row of ITEMS positions
   W v[ITEMS];
@@ -379,10 +391,26 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
     __syncwarp(1u);
   }
   __syncthreads();
+  // write-out: key i*THREADS + tid; its swizzle term ((i*THREADS + tid) /
+  // ITEMS) & 7 is per-thread constant when THREADS/ITEMS is a multiple of 8,
+  // so the loads take immediate offsets; full rounds carry no bounds test
+  {
+    constexpr int RPI = THREADS / ITEMS;
+    const int nfull = size / THREADS;  // block-uniform
+    const int trow = tid >> BS::kLogItems;
+    // the swizzle only touches bits below 32*KPC <= THREADS, so
+    // (i*THREADS + tid) ^ sw == i*THREADS + (tid ^ sw)
+    const int e0 = tid ^ ((trow & 7) << BS::kLogKpc);
+    const int e1 = tid ^ (((RPI + trow) & 7) << BS::kLogKpc);
+    W* d = dst + tid;
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int idx = i * THREADS + tid;
-    if (idx < size) dst[idx] = dec_x<FLT>(sk[BS::swz(idx)], X);
+    for (int i = 0; i < ITEMS; ++i) {
+      if (i >= nfull) break;
+      const int e = (RPI % 8 == 0 || (i * RPI) % 8 == 0) ? e0 : ((i * RPI) % 8 == RPI % 8 ? e1 : tid ^ (((i * RPI + trow) & 7) << BS::kLogKpc));
+      d[i * THREADS] = dec_x<FLT>(sk[i * THREADS + e], X);
+    }
+    const int idx = nfull * THREADS + tid;
+    if (nfull < ITEMS && idx < size) d[nfull * THREADS] = dec_x<FLT>(sk[BS::swz(idx)], X);
   }
   __syncthreads();
   return true;

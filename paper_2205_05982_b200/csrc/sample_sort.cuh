@@ -1235,17 +1235,21 @@ __global__ void __launch_bounds__(SortClass<CLS>::T, final_min_blocks<W, CLS>())
     const W* src = (item.flags & F_IN_B) ? P.b : P.a;
     const int size = (int)item.size;
     W k[ITEMS];
+    // padding: the maximum for the network (class 0); a copy of the item's
+    // first key for the counting sort (neutral for its min / max)
     if (item.flags & F_RAW) {  // only the root item of a small input is raw
+      const W pad = CLS >= 1 ? enc<W>(ldg(src + item.start), P.xf) : key_max<W>();
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
         const int idx = i * THREADS + threadIdx.x;
-        k[i] = idx < size ? enc<W>(ldcs(src + item.start + idx), P.xf) : key_max<W>();
+        k[i] = idx < size ? enc<W>(ldcs(src + item.start + idx), P.xf) : pad;
       }
     } else {
+      const W pad = CLS >= 1 ? ldg(src + item.start) : key_max<W>();
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
         const int idx = i * THREADS + threadIdx.x;
-        k[i] = idx < size ? ldcs(src + item.start + idx) : key_max<W>();
+        k[i] = idx < size ? ldcs(src + item.start + idx) : pad;
       }
     }
     W* dst = P.a + item.start;
