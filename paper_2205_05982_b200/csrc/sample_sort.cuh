@@ -82,12 +82,12 @@ struct Cfg {
 };
 template <>
 struct Cfg<unsigned long long> {
-  static constexpr int kTile = 2048;
-  static constexpr int kHistThreads = 256;
-  static constexpr int kScatThreads = 256;
+  static constexpr int kTile = 4096;
+  static constexpr int kHistThreads = 512;
+  static constexpr int kScatThreads = 512;
   static constexpr int kHistCopies = 1;
-  static constexpr int kScatMinBlocks = 4;
-  static constexpr int kHistMinBlocks = 5;
+  static constexpr int kScatMinBlocks = 2;
+  static constexpr int kHistMinBlocks = 2;
   static constexpr int kCap = 8192;
 };
 template <>
