@@ -296,7 +296,12 @@ def roofline(prof, stats, n, kb, peak):
             l, ms = prof[k]
             per_kernel[k] = {"launches": l, "ms": ms, "bytes_per_sort": bytes_[k]}
     if fin_l:
-        per_kernel["k_final"] = {"launches": fin_l, "ms": fin_ms, "bytes_per_sort": bytes_["k_final"]}
+        # the base case is one phase launched per size class (most classes
+        # are near-empty): count it as one launch per sort so the bytes of the
+        # whole phase are divided by the whole phase's time
+        sorts = prof.get("k_init", (fin_l, 0.0))[0]
+        per_kernel["k_final"] = {"launches": sorts, "ms": fin_ms, "bytes_per_sort": bytes_["k_final"],
+                                 "class_launches": fin_l}
     return per_kernel
 
 

@@ -272,6 +272,13 @@ __device__ __forceinline__ unsigned radix_digit(unsigned long long x, unsigned l
   const unsigned long long f = ((x > lo ? x : lo) - lo) >> shift;
   return umin(__umulhi((f >> 32) ? 0xFFFFFFFFu : (unsigned)f, mul), m);
 }
+// 64-bit keys whose bucket range spans >= 56 bits (shift >= 32): only the
+// high word of x - lo matters, and it never needs saturation.
+__device__ __forceinline__ unsigned radix_digit_hi(unsigned long long x, unsigned long long lo, int shift,
+                                                   unsigned mul, unsigned m) {
+  const unsigned f = (unsigned)((x - lo) >> 32) >> (shift - 32);
+  return umin(__umulhi(x < lo ? 0u : f, mul), m);
+}
 __device__ __forceinline__ unsigned radix_digit(const U128& x, const U128& lo, int shift, unsigned mul, unsigned m) {
   if (key_lt(x, lo)) return 0u;
   return umin(__umulhi(key_shr32(key_sub(x, lo), shift), mul), m);
@@ -283,7 +290,8 @@ struct SplSmem {
   W tree[256];  // implicit BST over srt[0..254] in BFS order (tree[1..255])
   W lo;
   unsigned cmax;
-  int shift, m, use_tree;  // use_tree: 0 table, 1 tree, 2 radix (equal-width digits)
+  int shift, m, use_tree;  // use_tree: 0 table, 1 tree, 2 radix (equal-width digits),
+                           //   3 radix on the high word (64-bit keys, shift >= 32)
   unsigned mul;  // radix mode multiplier (radix_digit)
   unsigned short lut[kLut];  // (first, end) splitter index of cell c, packed lo | hi << 8
 };
@@ -320,7 +328,7 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, unsigned lraw, Sp
       S.shift = (int)((lraw >> 16) & 0xFFu);
       S.m = m;
       S.mul = (unsigned)aux;
-      S.use_tree = 2;
+      S.use_tree = (sizeof(W) == 8 && S.shift >= 32) ? 3 : 2;
     }
     __syncthreads();
     return;
@@ -379,7 +387,9 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, unsigned lraw, Sp
 // lands in equality bucket 2m+1).
 template <int MODE, typename W>
 __device__ __forceinline__ int classify_mode(const W& x, const SplSmem<W>& S) {
-  if constexpr (MODE == 2) {
+  if constexpr (MODE == 3 && sizeof(W) == 8) {
+    return 2 * (int)radix_digit_hi(x, S.lo, S.shift, S.mul, (unsigned)S.m);
+  } else if constexpr (MODE >= 2) {
     // equal-width digits over the sample range (the sample certified them
     // balanced); keys below/above the range clamp to the first/last digit
     return 2 * (int)radix_digit(x, S.lo, S.shift, S.mul, (unsigned)S.m);
@@ -422,7 +432,9 @@ struct RadixReg {
 
 template <typename W>
 __device__ __forceinline__ int classify_fast(const W& x, const SplSmem<W>& S) {
-  return S.use_tree == 2 ? classify_mode<2>(x, S) : (S.use_tree ? classify_mode<1>(x, S) : classify_mode<0>(x, S));
+  return S.use_tree == 3 ? classify_mode<3>(x, S)
+                        : S.use_tree == 2 ? classify_mode<2>(x, S)
+                                          : (S.use_tree ? classify_mode<1>(x, S) : classify_mode<0>(x, S));
 }
 
 template <typename W>
@@ -737,7 +749,7 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
     auto count_tile = [&](auto tree_tag, auto flt_tag) {
       constexpr int TREE = decltype(tree_tag)::value;
       constexpr bool FLT = decltype(flt_tag)::value;
-      if (cnt == TILE && TREE == 2) {  // radix: stream classify -> count
+      if (cnt == TILE && TREE >= 2) {  // radix: stream classify -> count
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i)
           atomicAdd(&hist[classify_mode<TREE>(enc_x<FLT>(lds_key<W>(kp, i * THREADS + threadIdx.x), X), S)], 1u);
@@ -773,7 +785,10 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
         }
       }
     };
-    if (S.use_tree == 2) {
+    if (sizeof(W) == 8 && S.use_tree == 3) {
+      if (X.flt) count_tile(std::integral_constant<int, 3>{}, std::true_type{});
+      else count_tile(std::integral_constant<int, 3>{}, std::false_type{});
+    } else if (S.use_tree >= 2) {
       if (X.flt) count_tile(std::integral_constant<int, 2>{}, std::true_type{});
       else count_tile(std::integral_constant<int, 2>{}, std::false_type{});
     } else if (S.use_tree) {
@@ -1091,7 +1106,10 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
         }
       }
     };
-    if (S.use_tree == 2) {
+    if (sizeof(W) == 8 && S.use_tree == 3) {
+      if (X.flt) classify_tile(std::integral_constant<int, 3>{}, std::true_type{});
+      else classify_tile(std::integral_constant<int, 3>{}, std::false_type{});
+    } else if (S.use_tree >= 2) {
       if (X.flt) classify_tile(std::integral_constant<int, 2>{}, std::true_type{});
       else classify_tile(std::integral_constant<int, 2>{}, std::false_type{});
     } else if (S.use_tree) {
