@@ -198,7 +198,10 @@ struct BinSort {
   // XORed with a strictly higher bit, so this is a bijection.
   static constexpr int kLogItems = ITEMS == 4 ? 2 : ITEMS == 8 ? 3 : ITEMS == 16 ? 4 : 5;
   static constexpr int kLogKpc = sizeof(W) == 2 ? 3 : sizeof(W) == 4 ? 2 : sizeof(W) == 8 ? 1 : 0;
-  __device__ static __forceinline__ int swz(int p) { return p ^ (((p >> kLogItems) & 7) << kLogKpc); }
+  // (rows of a single chunk are consecutive chunks already: no swizzle)
+  static constexpr int kNV = ITEMS * (int)sizeof(W) / 16;
+  static constexpr int kSwz = kNV >= 2 ? 7 : 0;
+  __device__ static __forceinline__ int swz(int p) { return p ^ (((p >> kLogItems) & kSwz) << kLogKpc); }
 };
 
 // Block min / max of k[] over all THREADS*ITEMS slots (the caller pads with
@@ -344,7 +347,7 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
     const uint4* row = reinterpret_cast<const uint4*>(sk);
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
-      const uint4 t = row[(tid * NV + q) ^ (tid & 7)];
+      const uint4 t = row[(tid * NV + q) ^ (tid & BS::kSwz)];
       memcpy(reinterpret_cast<char*>(v) + 16 * q, &t, 16);
     }
   }
@@ -367,7 +370,7 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
     for (int q = 0; q < NV; ++q) {
       uint4 t;
       memcpy(&t, reinterpret_cast<const char*>(v) + 16 * q, 16);
-      row[(tid * NV + q) ^ (tid & 7)] = t;
+      row[(tid * NV + q) ^ (tid & BS::kSwz)] = t;
     }
   }
   __syncthreads();
@@ -400,13 +403,14 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
     const int trow = tid >> BS::kLogItems;
     // the swizzle only touches bits below 32*KPC <= THREADS, so
     // (i*THREADS + tid) ^ sw == i*THREADS + (tid ^ sw)
-    const int e0 = tid ^ ((trow & 7) << BS::kLogKpc);
-    const int e1 = tid ^ (((RPI + trow) & 7) << BS::kLogKpc);
+    const int e0 = tid ^ ((trow & BS::kSwz) << BS::kLogKpc);
+    const int e1 = tid ^ (((RPI + trow) & BS::kSwz) << BS::kLogKpc);
     W* d = dst + tid;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       if (i >= nfull) break;
-      const int e = (RPI % 8 == 0 || (i * RPI) % 8 == 0) ? e0 : ((i * RPI) % 8 == RPI % 8 ? e1 : tid ^ (((i * RPI + trow) & 7) << BS::kLogKpc));
+      const int e = (RPI % 8 == 0 || (i * RPI) % 8 == 0) ? e0
+                    : ((i * RPI) % 8 == RPI % 8 ? e1 : tid ^ (((i * RPI + trow) & BS::kSwz) << BS::kLogKpc));
       d[i * THREADS] = dec_x<FLT>(sk[i * THREADS + e], X);
     }
     const int idx = nfull * THREADS + tid;

@@ -1227,12 +1227,15 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   }
 }
 
-// Register budget of the counting-sort classes: 64 (<= 4-byte keys), 80
-// (8-byte) or 128 (16-byte) registers per thread, so several CTAs share an SM
-// and hide each other's item loads.
+// Register budget of the counting-sort classes (8 or 16 keys per thread):
+// 40/64 (<= 4-byte keys), 64/80 (8-byte) or 128 (16-byte) registers per
+// thread, so several CTAs share an SM and hide each other's item loads.
 template <typename W, int CLS>
 constexpr int final_min_blocks() {
-  return CLS == 0 ? 1 : (sizeof(W) <= 4 ? 1024 : sizeof(W) == 8 ? 768 : 512) / SortClass<CLS>::T;
+  constexpr int I = SortClass<CLS>::I;
+  constexpr int R = sizeof(W) <= 4 ? (I <= 8 ? 40 : 64) : sizeof(W) == 8 ? (I <= 8 ? 64 : 80) : 128;
+  constexpr int B = 65536 / (SortClass<CLS>::T * R);
+  return CLS == 0 ? 1 : (B < 1 ? 1 : B);
 }
 
 // Base case over one size class: load <= T*I keys (pad: transformed maximum),
