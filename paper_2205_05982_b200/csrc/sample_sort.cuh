@@ -509,6 +509,8 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
   W* s = reinterpret_cast<W*>(smem_raw);
   __shared__ unsigned dcnt[1 << kMaxRadixL];
   __shared__ unsigned s_maxc;
+  __shared__ W s_red_lo[THREADS / 32];
+  __shared__ W s_red_hi[THREADS / 32];
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
   const int nb = (int)(packed >> 40);
   if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrl->split_packed[P.cur ^ 1] = 0;
@@ -537,21 +539,17 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
       }
     }
     __syncthreads();
-    // sort the S samples (padded to 4096 with the maximum) with the block
-    // base-case sort, 512 threads x 8 keys, then stage them back to smem
+    // sample min / max (the radix certification needs no sorted sample)
+    W slo, shi;
     {
       constexpr int SI = kMaxSamples / THREADS;
       W k[SI];
 #pragma unroll
       for (int i = 0; i < SI; ++i) {
         const int idx = i * THREADS + threadIdx.x;
-        k[i] = idx < S ? s[idx] : key_max<W>();
+        k[i] = s[idx < S ? idx : 0];
       }
-      __syncthreads();
-      block_sort<W, THREADS, SI, sizeof(W) <= 4>(k, s);
-#pragma unroll
-      for (int i = 0; i < SI; ++i) s[threadIdx.x * SI + i] = k[i];
-      __syncthreads();
+      block_minmax<W, THREADS, SI>(k, slo, shi, s_red_lo, s_red_hi);
     }
     W* g = P.splitters + (unsigned long long)p * 256;
     const int step = S / (m + 1);
@@ -559,8 +557,7 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
     // give no digit more than ~2x its share of the sample, classify by digit
     // (pure ALU) instead of by splitter search.  Radix buckets may split up
     // to 2^kMaxRadixL ways (no splitter table is needed).
-    const W slo = s[0];
-    const W srange = key_sub(s[S - 1], slo);
+    const W srange = key_sub(shi, slo);
     const int bl = key_bitlen(srange);
     const int dshift = bl > 24 ? bl - 24 : 0;  // f = top 24 bits of (x - lo)
     const unsigned long long rf = key_shr32(srange, dshift);
@@ -614,6 +611,22 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
     if (radix) {
       if (threadIdx.x == 0) g[0] = slo;
     } else {
+      // sort the S samples (padded to 4096 with the maximum) with the block
+      // base-case sort, 512 threads x 8 keys, then stage them back to smem
+      {
+        constexpr int SI = kMaxSamples / THREADS;
+        W k[SI];
+#pragma unroll
+        for (int i = 0; i < SI; ++i) {
+          const int idx = i * THREADS + threadIdx.x;
+          k[i] = idx < S ? s[idx] : key_max<W>();
+        }
+        __syncthreads();
+        block_sort<W, THREADS, SI, sizeof(W) <= 4>(k, s);
+#pragma unroll
+        for (int i = 0; i < SI; ++i) s[threadIdx.x * SI + i] = k[i];
+        __syncthreads();
+      }
       // Equidistant splitters, deduplicated: low-entropy samples (few
       // distinct values) get a short splitter list, so the lookup table has
       // one splitter per cell and every key takes the fast path.
