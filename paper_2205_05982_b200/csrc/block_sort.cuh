@@ -219,6 +219,57 @@ template <typename W, int THREADS, int ITEMS>
 __device__ __forceinline__ void block_minmax(const W (&k)[ITEMS], W& lo, W& hi, W* red_lo, W* red_hi) {
   constexpr int NW = THREADS / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if constexpr (sizeof(W) == 8) {
+    // 64-bit keys: bounds from the 32-bit high words (two VIMNMX per key);
+    // only when every key shares one high word are the low words reduced.
+    // [lo, hi] then brackets the keys, which is all the binning needs.
+    unsigned* rl = reinterpret_cast<unsigned*>(red_lo);
+    unsigned* rh = reinterpret_cast<unsigned*>(red_hi);
+    auto reduce = [&](unsigned a, unsigned b, int slot, unsigned& oa, unsigned& ob) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        a = umin(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = umax(b, __shfl_xor_sync(0xffffffffu, b, o));
+      }
+      if (lane == 0) {
+        rl[2 * warp + slot] = a;
+        rh[2 * warp + slot] = b;
+      }
+      __syncthreads();
+      oa = rl[slot];
+      ob = rh[slot];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) {
+        oa = umin(oa, rl[2 * w + slot]);
+        ob = umax(ob, rh[2 * w + slot]);
+      }
+    };
+    unsigned a = (unsigned)(k[0] >> 32), b = a;
+#pragma unroll
+    for (int i = 1; i < ITEMS; ++i) {
+      a = umin(a, (unsigned)(k[i] >> 32));
+      b = umax(b, (unsigned)(k[i] >> 32));
+    }
+    unsigned mh, xh;
+    reduce(a, b, 0, mh, xh);
+    if (mh != xh) {  // block-uniform
+      lo = W((unsigned long long)mh << 32);
+      hi = W(((unsigned long long)xh << 32) | 0xFFFFFFFFull);
+      return;
+    }
+    a = (unsigned)k[0];
+    b = a;
+#pragma unroll
+    for (int i = 1; i < ITEMS; ++i) {
+      a = umin(a, (unsigned)k[i]);
+      b = umax(b, (unsigned)k[i]);
+    }
+    unsigned ml, xl;
+    reduce(a, b, 1, ml, xl);
+    lo = W(((unsigned long long)mh << 32) | ml);
+    hi = W(((unsigned long long)mh << 32) | xl);
+    return;
+  }
   lo = k[0];
   hi = k[0];
 #pragma unroll
