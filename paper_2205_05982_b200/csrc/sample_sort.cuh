@@ -78,6 +78,7 @@ struct Cfg {
   static constexpr int kHistCopies = 1;
   static constexpr int kScatMinBlocks = 2;
   static constexpr int kHistMinBlocks = 2;
+  static constexpr int kHistStages = 3;  // two tiles in flight while one is counted
   static constexpr int kCap = 8192;
 };
 template <>
@@ -88,6 +89,7 @@ struct Cfg<unsigned long long> {
   static constexpr int kHistCopies = 1;
   static constexpr int kScatMinBlocks = 2;
   static constexpr int kHistMinBlocks = 2;
+  static constexpr int kHistStages = 2;  // (3 would cost an SM's second CTA)
   static constexpr int kCap = 8192;
 };
 template <>
@@ -98,6 +100,7 @@ struct Cfg<uint16_t> {
   static constexpr int kHistCopies = 1;
   static constexpr int kScatMinBlocks = 1;
   static constexpr int kHistMinBlocks = 2;
+  static constexpr int kHistStages = 3;
   static constexpr int kCap = 8192;
 };
 template <>
@@ -108,9 +111,10 @@ struct Cfg<U128> {
   static constexpr int kHistCopies = 1;
   static constexpr int kScatMinBlocks = 2;
   static constexpr int kHistMinBlocks = 4;
+  static constexpr int kHistStages = 2;
   static constexpr int kCap = 4096;
 };
-constexpr int kStages = 2;  // TMA tile pipeline depth
+constexpr int kStages = 2;  // TMA tile pipeline depth (k_scatter; k_hist uses Cfg::kHistStages)
 
 // Base-case classes (THREADS, ITEMS); capacity THREADS*ITEMS.  The smallest
 // class merges inside the warp with the __shfl_xor_sync network (WARP_NET).
@@ -696,8 +700,8 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
   constexpr int ITEMS = TILE / THREADS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ SplSmem<W> S;
-  __shared__ unsigned hist[kChildStride];
-  __shared__ __align__(8) unsigned long long bars[kStages];
+  __shared__ unsigned hist[kChildStride + 1];  // + dump slot
+  __shared__ __align__(8) unsigned long long bars[Cfg<W>::kHistStages];
   __shared__ int s_p;
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
   const int nb = (int)(packed >> 40);
@@ -711,11 +715,15 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
   int p_issue = 0;
   if (threadIdx.x == 0) {
     s_p = find_bucket(list, nb, t0);
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < Cfg<W>::kHistStages; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     p_issue = s_p;
-    const TileRef r = tile_ref<W>(list, nb, p_issue, t0);
-    tile_issue(src_of(P, list[r.p].flags) + r.lo, (unsigned long long)r.cnt * sizeof(W), smem_raw, &bars[0]);
+    for (int s = 0; s + 1 < Cfg<W>::kHistStages && t0 + s < t1; ++s) {  // prefetch depth Cfg<W>::kHistStages - 1
+      const TileRef r = tile_ref<W>(list, nb, p_issue, t0 + s);
+      p_issue = r.p;
+      tile_issue(src_of(P, list[r.p].flags) + r.lo, (unsigned long long)r.cnt * sizeof(W),
+                 smem_raw + s * stage_bytes<W>(), &bars[s]);
+    }
   }
   for (int i = threadIdx.x; i < kChildStride; i += THREADS) hist[i] = 0;
   __syncthreads();
@@ -724,13 +732,15 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
   int L = (int)(d.L & 0xFFu);
   load_splitters(P.splitters + (unsigned long long)p * 256, d.L, S, d.aux);
   unsigned phase = 0;
-  for (unsigned long long t = t0; t < t1; ++t) {
-    const int st = (int)((t - t0) & (kStages - 1));
-    if (threadIdx.x == 0 && t + 1 < t1) {
-      const TileRef r = tile_ref<W>(list, nb, p_issue, t + 1);
+  int st = 0;  // stage of tile t
+  for (unsigned long long t = t0; t < t1; ++t, st = st + 1 == Cfg<W>::kHistStages ? 0 : st + 1) {
+    if (threadIdx.x == 0 && t + Cfg<W>::kHistStages - 1 < t1) {
+      // the stage consumed in the previous iteration (freed by its final barrier)
+      const int sn = st == 0 ? Cfg<W>::kHistStages - 1 : st - 1;
+      const TileRef r = tile_ref<W>(list, nb, p_issue, t + Cfg<W>::kHistStages - 1);
       p_issue = r.p;
       tile_issue(src_of(P, list[r.p].flags) + r.lo, (unsigned long long)r.cnt * sizeof(W),
-                 smem_raw + (st ^ 1) * stage_bytes<W>(), &bars[st ^ 1]);
+                 smem_raw + sn * stage_bytes<W>(), &bars[sn]);
     }
     if (p + 1 < nb && list[p + 1].tile_base <= t) {
       // flush and move to the next bucket
@@ -781,9 +791,9 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
           if ((threadIdx.x & 31) == 0) atomicAdd(&hist[b0], 32u * ITEMS);
         } else {
 #pragma unroll
-          for (int i = 0; i < ITEMS; ++i) {
-            if (bk[i] >= 0) atomicAdd(&hist[bk[i]], 1u);
-            else wide |= 1u << i;
+          for (int i = 0; i < ITEMS; ++i) {  // (wide cells count into a dump slot)
+            atomicAdd(&hist[bk[i] >= 0 ? bk[i] : kChildStride], 1u);
+            wide |= (bk[i] < 0 ? 1u : 0u) << i;
           }
         }
       } else {
@@ -1148,6 +1158,9 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       base = __shfl_sync(0xffffffffu, base, 0) + lane * ITEMS;
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) bk[i] = (b0 << 16) | (int)(base + i);
+    } else if (cnt == TILE) {  // full tile: every id is valid (straight-line code)
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) bk[i] = (bk[i] << 16) | (int)atomicAdd(&myhist[bk[i]], 1u);
     } else {
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i)
@@ -1194,10 +1207,21 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       }
       __syncthreads();
       W* staged = reinterpret_cast<W*>(stage);
-      if (radix) {  // child ids are recomputed from the keys at write-out
+      if (radix && cnt == TILE) {  // child ids are recomputed from the keys at write-out
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) staged[myhist[bk[i] >> 16] + (unsigned)(bk[i] & 0xFFFF)] = k[i];
+      } else if (radix) {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
           if (bk[i] >= 0) staged[myhist[bk[i] >> 16] + (unsigned)(bk[i] & 0xFFFF)] = k[i];
+        }
+      } else if (cnt == TILE) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const int c = bk[i] >> 16;
+          const unsigned pos = myhist[c] + (unsigned)(bk[i] & 0xFFFF);
+          staged[pos] = k[i];
+          stage_b[pos] = (unsigned short)c;
         }
       } else {
 #pragma unroll
@@ -1218,7 +1242,21 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     }
     W* staged = reinterpret_cast<W*>(stage);
     __syncthreads();
-    if (radix) {
+    if (radix && out_xf == XF_NONE && cnt == TILE) {  // full tile: unrolled, no bounds
+      const RadixReg<W> R(S);
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int j = i * THREADS + threadIdx.x;
+        const W v = staged[j];
+        dst_buf[gdelta[R.child(v)] + j] = v;
+      }
+    } else if (out_xf == XF_NONE && cnt == TILE) {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int j = i * THREADS + threadIdx.x;
+        dst_buf[gdelta[stage_b[j]] + j] = staged[j];
+      }
+    } else if (radix) {
       const RadixReg<W> R(S);
       if (out_xf == XF_NONE) {
         for (int j = threadIdx.x; j < cnt; j += THREADS) {

@@ -218,7 +218,7 @@ constexpr size_t sample_smem() {
 }
 template <typename W>
 constexpr size_t hist_smem() {
-  return (size_t)kStages * stage_bytes<W>();
+  return (size_t)Cfg<W>::kHistStages * stage_bytes<W>();
 }
 template <typename W>
 constexpr size_t scatter_smem() {
