@@ -136,6 +136,30 @@ vxs_status vxs_partition(const void* d_keys, size_t n, vxs_key_type type, vxs_or
                          const void* d_splitters, int nspl, void* d_out, uint64_t* d_seg_counts,
                          void* d_workspace, size_t workspace_bytes, void* stream);
 
+/* Fused exchange for the distributed sort: a partition split
+ * in two so the all-to-all rides on the scatter's own stores.
+ * vxs_partition_counts: phase 1 (read-only): per-segment counts of d_keys by
+ *   the splitters into d_seg_counts; the (required) workspace keeps the
+ *   per-CTA offsets for phase 2.
+ * vxs_partition_exchange: phase 2: segment i's keys (original encoding) are
+ *   stored at ((key*)d_dst[i]) + d_dst_offsets[i] -- device arrays of nspl+1
+ *   addresses / element offsets, typically peers' receive buffers mapped with
+ *   vxs_ipc_open.  Same keys, n, type, order, nspl and workspace as phase 1.
+ * vxs_device_alloc / vxs_device_free: IPC-exportable device blocks.
+ * vxs_ipc_handle: 64-byte cudaIpcMemHandle_t of a vxs_device_alloc block.
+ * vxs_ipc_open / vxs_ipc_close: map / unmap a peer's block (P2P). */
+vxs_status vxs_partition_counts(const void* d_keys, size_t n, vxs_key_type type, vxs_order order,
+                                const void* d_splitters, int nspl, uint64_t* d_seg_counts, void* d_workspace,
+                                size_t workspace_bytes, void* stream);
+vxs_status vxs_partition_exchange(const void* d_keys, size_t n, vxs_key_type type, vxs_order order, int nspl,
+                                  const uint64_t* d_dst, const uint64_t* d_dst_offsets, void* d_workspace,
+                                  size_t workspace_bytes, void* stream);
+vxs_status vxs_device_alloc(size_t bytes, void** d_ptr);
+vxs_status vxs_device_free(void* d_ptr);
+vxs_status vxs_ipc_handle(void* d_ptr, void* handle64);
+vxs_status vxs_ipc_open(const void* handle64, void** d_ptr);
+vxs_status vxs_ipc_close(void* d_ptr);
+
 /* Key transform as used inside the kernels (exposed for tests): encodes
  * (inverse=0) or decodes (inverse=1) n keys in place on the device. */
 vxs_status vxs_transform(void* d_keys, size_t n, vxs_key_type type, vxs_order order, int inverse,

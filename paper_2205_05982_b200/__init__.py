@@ -139,9 +139,17 @@ def lib():
         L.vxs_argsort_workspace_bytes.argtypes = [sz, i, sz, ctypes.POINTER(ctypes.c_size_t)]
         L.vxs_argsort.argtypes = [vp, sz, i, i, vp, vp, u64, i, vp, sz, vp, ctypes.POINTER(SortStats)]
         L.vxs_sort_pairs.argtypes = [vp, vp, sz, sz, i, i, u64, i, vp, sz, vp, ctypes.POINTER(SortStats)]
+        L.vxs_partition_counts.argtypes = [vp, sz, i, i, vp, i, vp, vp, sz, vp]
+        L.vxs_partition_exchange.argtypes = [vp, sz, i, i, i, vp, vp, vp, sz, vp]
+        L.vxs_device_alloc.argtypes = [sz, ctypes.POINTER(ctypes.c_void_p)]
+        L.vxs_device_free.argtypes = [vp]
+        L.vxs_ipc_handle.argtypes = [vp, vp]
+        L.vxs_ipc_open.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p)]
+        L.vxs_ipc_close.argtypes = [vp]
         for fn in ("vxs_sort", "vxs_sort_host", "vxs_sort_workspace_bytes", "vxs_sample",
                    "vxs_partition", "vxs_transform", "vxs_argsort_workspace_bytes", "vxs_argsort",
-                   "vxs_sort_pairs"):
+                   "vxs_sort_pairs", "vxs_partition_counts", "vxs_partition_exchange", "vxs_device_alloc",
+                   "vxs_device_free", "vxs_ipc_handle", "vxs_ipc_open", "vxs_ipc_close"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -151,7 +159,9 @@ EXPORTED_SYMBOLS = ["vxs_sort_workspace_bytes", "vxs_sort", "vxs_sort_host", "vx
                     "vxs_partition", "vxs_transform", "vxs_argsort_workspace_bytes", "vxs_argsort",
                     "vxs_sort_pairs", "vxs_sort_range", "vxs_last_error", "vxs_key_bytes",
                     "vxs_base_case_capacity", "vxs_version", "vxs_profile_enable",
-                    "vxs_profile_reset", "vxs_profile_read"]
+                    "vxs_profile_reset", "vxs_profile_read", "vxs_partition_counts",
+                    "vxs_partition_exchange", "vxs_device_alloc", "vxs_device_free", "vxs_ipc_handle",
+                    "vxs_ipc_open", "vxs_ipc_close"]
 
 
 class KernelProfile(ctypes.Structure):
@@ -378,6 +388,73 @@ def partition(keys, splitters, order: Order = Order.kAscending, key_type=None, o
                                splitters.data_ptr() if nspl else None, nspl, out.data_ptr(),
                                counts.data_ptr(), None, 0, _stream_ptr(stream)))
     return out, counts
+
+
+def partition_counts(keys, splitters, workspace, order: Order = Order.kAscending, key_type=None, stream=None):
+    """Fused-exchange phase 1 (vxs_partition_counts): per-segment counts
+    (int64 tensor of nspl+1); `workspace` (uint8 device tensor of
+    workspace_bytes(n, key_type)) keeps the offsets for phase 2."""
+    import torch
+    kt = infer_key_type(keys, key_type)
+    n = _nkeys(keys, kt)
+    nspl = int(splitters.shape[0])
+    counts = torch.zeros(nspl + 1, dtype=torch.int64, device=keys.device)
+    _check(lib().vxs_partition_counts(keys.data_ptr(), n, KEY_CODE[kt], int(order),
+                                      splitters.data_ptr() if nspl else None, nspl, counts.data_ptr(),
+                                      workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)))
+    return counts
+
+
+def partition_exchange(keys, nspl: int, dst_addrs, dst_offsets, workspace, order: Order = Order.kAscending,
+                       key_type=None, stream=None):
+    """Fused-exchange phase 2 (vxs_partition_exchange): segment i's keys are
+    stored at element dst_offsets[i] of the buffer at address dst_addrs[i]
+    (int64 device tensors of nspl+1 entries; peers' receive buffers)."""
+    kt = infer_key_type(keys, key_type)
+    _check(lib().vxs_partition_exchange(keys.data_ptr(), _nkeys(keys, kt), KEY_CODE[kt], int(order), int(nspl),
+                                        dst_addrs.data_ptr(), dst_offsets.data_ptr(), workspace.data_ptr(),
+                                        workspace.numel(), _stream_ptr(stream)))
+
+
+class DeviceBlock:
+    """An IPC-exportable device allocation (vxs_device_alloc) viewed as a
+    torch tensor through __cuda_array_interface__; `handle()` is its 64-byte
+    CUDA IPC handle, `DeviceBlock.open(handle, ...)` maps a peer's block."""
+
+    def __init__(self, nbytes: int, ptr: Optional[int] = None, owned: bool = True):
+        self.nbytes = int(nbytes)
+        self.owned = owned
+        if ptr is None:
+            out = ctypes.c_void_p()
+            _check(lib().vxs_device_alloc(max(self.nbytes, 16), ctypes.byref(out)))
+            ptr = out.value
+        self.ptr = int(ptr)
+
+    @classmethod
+    def open(cls, handle: bytes, nbytes: int) -> "DeviceBlock":
+        out = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(bytes(handle), 64)
+        _check(lib().vxs_ipc_open(buf, ctypes.byref(out)))
+        return cls(nbytes, ptr=out.value, owned=False)
+
+    def handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        _check(lib().vxs_ipc_handle(ctypes.c_void_p(self.ptr), buf))
+        return buf.raw
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self.nbytes,), "typestr": "|u1", "data": (self.ptr, False), "version": 3}
+
+    def tensor(self):
+        import torch
+        return torch.as_tensor(self, device="cuda")
+
+    def close(self):
+        if self.ptr:
+            _check(lib().vxs_device_free(ctypes.c_void_p(self.ptr)) if self.owned
+                   else lib().vxs_ipc_close(ctypes.c_void_p(self.ptr)))
+            self.ptr = 0
 
 
 def transform(keys, order: Order = Order.kAscending, inverse=False, key_type=None, stream=None):

@@ -187,6 +187,11 @@ struct Params {
   // full sort).  Children whose final range misses [rlo, rhi) are not split
   // or sorted further -- only moved back into A (nth_element / partial_sort).
   unsigned long long rlo, rhi;
+  // vxs_partition_exchange: segment i is written to ((W*)xdst[i]) + xoff[i]
+  // (a peer's receive buffer over NVLink, or a local one); 0 = off
+  int xchg;
+  const unsigned long long* xdst;
+  const unsigned long long* xoff;
 };
 
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
@@ -1034,7 +1039,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   constexpr int HC = Cfg<W>::kHistCopies;  // histogram copies (warp w uses copy w % HC)
   unsigned* whist = reinterpret_cast<unsigned*>(stage_b + TILE);  // [HC][kChildStride]
   __shared__ SplSmem<W> S;
-  __shared__ long long gdelta[kChildStride];  // global index of staged slot 0 of child c
+  __shared__ W* gptr[kChildStride];  // where staged slot 0 of child c goes (slot j -> gptr[c][j])
   __shared__ unsigned long long gcur[kChildStride];  // this CTA's next global slot per child
   __shared__ unsigned scan_scratch[32];
   __shared__ __align__(8) unsigned long long bars[kStages];
@@ -1237,7 +1242,16 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
         const int c = threadIdx.x * PER + j;
-        if (tot[j] && c < nc) gdelta[c] = (long long)gres[j] - (long long)exc[j];
+        if (tot[j] && c < nc) {
+          // (vxs_partition_exchange: segment c/2 goes straight to its owner's
+          // receive buffer at this rank's offset there -- the fused exchange)
+          W* base = dst_buf;
+          if (P.xchg) {
+            const int sg = c >> 1;
+            base = reinterpret_cast<W*>(P.xdst[sg]) + P.xoff[sg] - P.childbase[2 * sg];
+          }
+          gptr[c] = base + ((long long)gres[j] - (long long)exc[j]);
+        }
       }
     }
     W* staged = reinterpret_cast<W*>(stage);
@@ -1248,34 +1262,35 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       for (int i = 0; i < ITEMS; ++i) {
         const int j = i * THREADS + threadIdx.x;
         const W v = staged[j];
-        dst_buf[gdelta[R.child(v)] + j] = v;
+        gptr[R.child(v)][j] = v;
       }
     } else if (out_xf == XF_NONE && cnt == TILE) {
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
         const int j = i * THREADS + threadIdx.x;
-        dst_buf[gdelta[stage_b[j]] + j] = staged[j];
+        gptr[stage_b[j]][j] = staged[j];
       }
     } else if (radix) {
       const RadixReg<W> R(S);
       if (out_xf == XF_NONE) {
         for (int j = threadIdx.x; j < cnt; j += THREADS) {
           const W v = staged[j];
-          dst_buf[gdelta[R.child(v)] + j] = v;
+          gptr[R.child(v)][j] = v;
         }
       } else {
         for (int j = threadIdx.x; j < cnt; j += THREADS) {
           const W v = staged[j];
-          dst_buf[gdelta[R.child(v)] + j] = dec<W>(v, out_xf);
+          gptr[R.child(v)][j] = dec<W>(v, out_xf);
         }
       }
     } else if (out_xf == XF_NONE) {
-      for (int j = threadIdx.x; j < cnt; j += THREADS) dst_buf[gdelta[stage_b[j]] + j] = staged[j];
+      for (int j = threadIdx.x; j < cnt; j += THREADS) gptr[stage_b[j]][j] = staged[j];
     } else {  // vxs_partition: decode into the caller's encoding
-      for (int j = threadIdx.x; j < cnt; j += THREADS) dst_buf[gdelta[stage_b[j]] + j] = dec<W>(staged[j], out_xf);
+      for (int j = threadIdx.x; j < cnt; j += THREADS) gptr[stage_b[j]][j] = dec<W>(staged[j], out_xf);
     }
     __syncthreads();
   }
+  if (P.xchg) __threadfence_system();  // peer stores visible before the exchange's barrier
 }
 
 // Register budget of the counting-sort classes (8 or 16 keys per thread):

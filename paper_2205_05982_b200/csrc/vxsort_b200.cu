@@ -1365,4 +1365,106 @@ vxs_status vxs_partition(const void* d_keys, size_t n, vxs_key_type type, vxs_or
   });
 }
 
+// Fused exchange, phase 1: the read-only half of a partition -- classify
+// every key by the splitters, per-(bucket, CTA) counts, offsets, per-segment
+// totals in d_seg_counts.  The workspace keeps that state for phase 2.
+vxs_status vxs_partition_counts(const void* d_keys, size_t n, vxs_key_type type, vxs_order order,
+                                const void* d_splitters, int nspl, uint64_t* d_seg_counts, void* d_workspace,
+                                size_t workspace_bytes, void* stream) {
+  if (!valid_order(order)) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: invalid order");
+  if (nspl < 0 || nspl > 255) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: nspl must be in [0, 255]");
+  if (d_workspace == nullptr) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: partition_counts needs a workspace");
+  const int xf = xform_for(type, order);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return with_word(type, [&](auto* tag) -> vxs_status {
+    using W = std::remove_pointer_t<decltype(tag)>;
+    const int nseg = nspl + 1;
+    if (n == 0) {
+      VXS_CK(cudaMemsetAsync(d_seg_counts, 0, nseg * sizeof(uint64_t), st), "memset");
+      return VXS_OK;
+    }
+    const Layout Lay = layout_for<W>(n);
+    if (workspace_bytes < Lay.total) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: provided workspace is too small");
+    Params<W> P = make_params<W>(const_cast<W*>(static_cast<const W*>(d_keys)), n, xf, 0,
+                                 static_cast<unsigned char*>(d_workspace), Lay);
+    P.part_mode = 1;
+    int L = 1;
+    while ((1 << L) - 1 < nspl) ++L;
+    k_init<W><<<1, 32, 0, st>>>(P);
+    k_part_setup<W><<<1, 256, 0, st>>>(P, static_cast<const W*>(d_splitters), nspl, L);
+    k_hist<W><<<P.grid, Cfg<W>::kHistThreads, hist_smem<W>(), st>>>(P);
+    k_segscan<W><<<16, 128, 0, st>>>(P);
+    k_plan<W><<<1, kChildStride, 0, st>>>(P);
+    k_part_counts<W><<<1, 256, 0, st>>>(P, nseg, reinterpret_cast<unsigned long long*>(d_seg_counts));
+    VXS_CK(cudaGetLastError(), "partition_counts");
+    return VXS_OK;
+  });
+}
+
+// Fused exchange, phase 2: the classify + scatter pass, with segment i's keys
+// stored straight into ((key type*)d_dst[i]) + d_dst_offsets[i] -- another
+// rank's receive buffer mapped over NVLink (vxs_ipc_open), so the
+// all-to-all rides on the scatter's own stores.  Same keys, n, type, order,
+// nspl and workspace as the phase-1 call; d_dst / d_dst_offsets are device
+// arrays of nspl+1 entries.  Ends with a system-scope fence per CTA.
+vxs_status vxs_partition_exchange(const void* d_keys, size_t n, vxs_key_type type, vxs_order order, int nspl,
+                                  const uint64_t* d_dst, const uint64_t* d_dst_offsets, void* d_workspace,
+                                  size_t workspace_bytes, void* stream) {
+  if (!valid_order(order)) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: invalid order");
+  if (nspl < 0 || nspl > 255) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: nspl must be in [0, 255]");
+  if (d_workspace == nullptr) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: partition_exchange needs a workspace");
+  const int xf = xform_for(type, order);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return with_word(type, [&](auto* tag) -> vxs_status {
+    using W = std::remove_pointer_t<decltype(tag)>;
+    if (n == 0) return VXS_OK;
+    const Layout Lay = layout_for<W>(n);
+    if (workspace_bytes < Lay.total) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: provided workspace is too small");
+    Params<W> P = make_params<W>(const_cast<W*>(static_cast<const W*>(d_keys)), n, xf, 0,
+                                 static_cast<unsigned char*>(d_workspace), Lay);
+    P.part_mode = 1;
+    P.xchg = 1;
+    P.xdst = reinterpret_cast<const unsigned long long*>(d_dst);
+    P.xoff = reinterpret_cast<const unsigned long long*>(d_dst_offsets);
+    {
+      ProfScope ps(K_PART, st);
+      k_scatter<W><<<P.grid, Cfg<W>::kScatThreads, scatter_smem<W>(), st>>>(P);
+    }
+    VXS_CK(cudaGetLastError(), "partition_exchange");
+    return VXS_OK;
+  });
+}
+
+// Symmetric receive buffers for the fused exchange: plain cudaMalloc blocks
+// (IPC-exportable), their 64-byte IPC handles, and peer mappings (P2P over
+// NVLink via cudaIpcMemLazyEnablePeerAccess).
+vxs_status vxs_device_alloc(size_t bytes, void** d_ptr) {
+  if (d_ptr == nullptr) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: null out pointer");
+  VXS_CK(cudaMalloc(d_ptr, bytes ? bytes : 16), "device alloc");
+  return VXS_OK;
+}
+vxs_status vxs_device_free(void* d_ptr) {
+  VXS_CK(cudaFree(d_ptr), "device free");
+  return VXS_OK;
+}
+vxs_status vxs_ipc_handle(void* d_ptr, void* handle64) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  if (handle64 == nullptr) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: null handle buffer");
+  cudaIpcMemHandle_t h;
+  VXS_CK(cudaIpcGetMemHandle(&h, d_ptr), "ipc get handle");
+  std::memcpy(handle64, &h, sizeof(h));
+  return VXS_OK;
+}
+vxs_status vxs_ipc_open(const void* handle64, void** d_ptr) {
+  if (handle64 == nullptr || d_ptr == nullptr) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  VXS_CK(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess), "ipc open handle");
+  return VXS_OK;
+}
+vxs_status vxs_ipc_close(void* d_ptr) {
+  VXS_CK(cudaIpcCloseMemHandle(d_ptr), "ipc close handle");
+  return VXS_OK;
+}
+
 }  // extern "C"

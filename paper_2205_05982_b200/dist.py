@@ -20,6 +20,19 @@ sizes, offsets) is plain Python so the world_size>1 path is tested on CPU
 with the gloo backend (tests/test_dist_gloo.py), where ``ops`` supplies CPU
 stand-ins for the three device kernels.  The product path always uses the
 CUDA ops (``CudaOps``) and fails loudly without them.
+
+Exchange (step 4) comes in two forms:
+  * ``exchange="fused"`` (default): the partition is split in
+    two -- ``vxs_partition_counts`` (read-only classify + per-CTA offsets),
+    an all-gather of the tiny G x G count matrix, then
+    ``vxs_partition_exchange``, whose scatter stores every segment straight
+    into its owner's receive buffer (a symmetric window: one IPC-exported
+    block per rank, mapped by every peer over NVLink) at this rank's offset
+    there.  The all-to-all rides on the scatter's own stores: no local
+    partitioned copy, no NCCL data movement; one small all-reduce orders the
+    peers' stores before the local sort.
+  * ``exchange="nccl"``: partition into a local buffer, then NCCL
+    ``all_to_all_single`` of counts and keys (the baseline).
 """
 from __future__ import annotations
 
@@ -28,11 +41,58 @@ from typing import Optional
 import torch
 import torch.distributed as dist
 
-from . import KEY_BYTES, Order, SortConfig, infer_key_type, partition, sample, sort
+from . import (KEY_BYTES, DeviceBlock, Order, SortConfig, infer_key_type, partition, partition_counts,
+               partition_exchange, sample, sort, workspace_bytes)
+
+
+class SymmetricWindow:
+    """Per-group receive buffers of the fused exchange: one IPC-exportable
+    device block per rank, each mapped by every peer (P2P over NVLink /
+    NVSwitch).  Capacity only grows, collectively (every rank computes the
+    same required size from the same all-gathered count matrix)."""
+
+    def __init__(self):
+        self.nbytes = 0
+        self.mine = None
+        self.peers = []   # DeviceBlock per rank (rank's own = self.mine)
+        self.addrs = None  # int64 device tensor of the ranks' base addresses
+
+    def ensure(self, nbytes: int, group, device):
+        if nbytes <= self.nbytes:
+            return
+        nbytes = max(nbytes, int(self.nbytes * 1.25))
+        nbytes = (nbytes + (1 << 21) - 1) & ~((1 << 21) - 1)
+        self.close()
+        torch.cuda.synchronize(device)
+        self.mine = DeviceBlock(nbytes)
+        handles = [None] * dist.get_world_size(group)
+        dist.all_gather_object(handles, self.mine.handle(), group=group)
+        me = dist.get_rank(group)
+        self.peers = [self.mine if r == me else DeviceBlock.open(h, nbytes) for r, h in enumerate(handles)]
+        self.addrs = torch.tensor([b.ptr for b in self.peers], dtype=torch.int64, device=device)
+        self.nbytes = nbytes
+
+    def local(self):
+        return self.mine.tensor()
+
+    def close(self):
+        for b in self.peers:
+            if b is not self.mine:
+                b.close()
+        if self.mine is not None:
+            self.mine.close()
+        self.peers, self.mine, self.nbytes = [], None, 0
+
+
+_WINDOWS = {}
+
+
+def _window(group) -> SymmetricWindow:
+    return _WINDOWS.setdefault(id(group), SymmetricWindow())
 
 
 class CudaOps:
-    """The three device kernels a rank runs (libvxsort_b200.so)."""
+    """The device kernels a rank runs (libvxsort_b200.so)."""
 
     def sample(self, keys, s, order, key_type, seed):
         return sample(keys, s, order=order, seed=seed, key_type=key_type)
@@ -50,6 +110,26 @@ class CudaOps:
         sort(keys, SortConfig(order=order, seed=1), key_type=key_type if key_type in ("k128", "kv64") else None)
         return keys
 
+    # fused exchange
+    def workspace(self, keys, key_type):
+        return torch.empty(workspace_bytes(max(1, keys.shape[0]), key_type), dtype=torch.uint8, device=keys.device)
+
+    def partition_counts(self, keys, splitters, order, key_type, ws):
+        return partition_counts(keys, splitters, ws, order=order, key_type=key_type)
+
+    def window(self, group):
+        return _window(group)
+
+    def exchange(self, keys, nspl, window, offsets, order, key_type, ws, group=None):
+        dev = window.addrs.device
+        if keys is not None and keys.shape[0] > 0:
+            offs = torch.as_tensor(offsets, dtype=torch.int64).to(dev, non_blocking=True)
+            partition_exchange(keys, nspl, window.addrs, offs, ws, order=order, key_type=key_type)
+        # order every peer's stores before anyone reads its window: a stream-
+        # ordered collective after the exchange kernel on every rank
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, group=group)
+
 
 def _bytes(t: torch.Tensor) -> torch.Tensor:
     if t.numel() == 0:
@@ -61,13 +141,32 @@ def choose_splitters(gathered_sorted: torch.Tensor, world: int, per_rank: int) -
     """G-1 equidistant global splitters from the sorted G*s sample (every rank
     computes the same ones from the same all-gathered bytes)."""
     idx = torch.arange(1, world, device=gathered_sorted.device) * per_rank - 1
-    return gathered_sorted[idx].contiguous()
+    # (CUDA indexing has no unsigned kernels: gather the same bits as signed)
+    signed = {torch.uint64: torch.int64, torch.uint32: torch.int32, torch.uint16: torch.int16}
+    t = gathered_sorted
+    if t.dtype in signed:
+        return t.view(signed[t.dtype])[idx].contiguous().view(t.dtype)
+    return t[idx].contiguous()
+
+
+def exchange_offsets(all_counts, rank: int):
+    """From the G x G count matrix (row s = rank s's per-destination counts):
+    this rank's element offset inside every destination's receive buffer
+    (senders land in rank order) and how many keys this rank receives."""
+    world = len(all_counts)
+    offs = [sum(all_counts[s][r] for s in range(rank)) for r in range(world)]
+    recv = sum(all_counts[s][rank] for s in range(world))
+    need = max(sum(all_counts[s][r] for s in range(world)) for r in range(world))
+    return offs, recv, need
 
 
 def dist_sort(local: torch.Tensor, order: Order = Order.kAscending, key_type: Optional[str] = None,
-              group=None, oversample: int = 256, seed: int = 1, ops=None, timings: Optional[dict] = None):
+              group=None, oversample: int = 256, seed: int = 1, ops=None, timings: Optional[dict] = None,
+              exchange: str = "fused", copy_out: bool = True):
     """Sort the union of every rank's ``local`` keys; returns this rank's
-    sorted slice of the global order (a new tensor)."""
+    sorted slice of the global order (a new tensor; with exchange="fused" and
+    copy_out=False, a view of the group's receive window that the next
+    dist_sort on the group overwrites)."""
     ops = ops or CudaOps()
     kt = infer_key_type(local, key_type)
     kb = KEY_BYTES[kt]
@@ -93,6 +192,8 @@ def dist_sort(local: torch.Tensor, order: Order = Order.kAscending, key_type: Op
     words = gathered.view(smp.dtype).reshape((world * s, 2) if kb == 16 else (world * s,)).clone()
     words = ops.sort_words(words, kb)
     spl = choose_splitters(words, world, s)
+    if exchange == "fused":
+        return _fused_tail(local, n, kt, kb, spl, order, group, world, rank, ops, timings, copy_out)
     # 3. local multiway partition into `world` segments
     if n > 0:
         parted, seg_counts = ops.partition(local, spl, order, kt)
@@ -115,3 +216,28 @@ def dist_sort(local: torch.Tensor, order: Order = Order.kAscending, key_type: Op
         timings["recv_keys"] = int(out.shape[0])
         timings["send_counts"] = seg_counts.tolist()
     return out
+
+
+def _fused_tail(local, n, kt, kb, spl, order, group, world, rank, ops, timings, copy_out):
+    """Steps 3-5 with the fused exchange (module docstring)."""
+    ws = ops.workspace(local, kt)
+    if n > 0:
+        counts = ops.partition_counts(local, spl, order, kt, ws)
+    else:
+        counts = torch.zeros(world, dtype=torch.int64, device=local.device)
+    allc = torch.empty(world * world, dtype=torch.int64, device=local.device)
+    dist.all_gather_into_tensor(allc, counts, group=group)
+    m = allc.view(world, world).tolist()
+    offs, recv, need = exchange_offsets(m, rank)
+    win = ops.window(group)
+    win.ensure(need * kb, group, local.device)
+    ops.exchange(local if n > 0 else None, world - 1, win, offs, order, kt, ws, group)
+    buf = win.local()[: recv * kb]
+    shape = (recv, 2) if kb == 16 else (recv,)
+    out = buf.view(local.dtype).reshape(shape)
+    if recv > 1:
+        out = ops.sort(out, order, kt)
+    if timings is not None:
+        timings["recv_keys"] = int(recv)
+        timings["send_counts"] = m[rank]
+    return out.clone() if copy_out else out

@@ -1,5 +1,6 @@
 """World-size-2 (and 3) CPU runs of the distributed sample sort's host logic
-over the gloo backend.  The three device kernels are replaced, in this test
+over the gloo backend, for both exchanges (NCCL-style all-to-all and the
+fused partition+exchange, whose peer stores are emulated here).  The three device kernels are replaced, in this test
 only, by CPU stand-ins built on the oracle; the collectives, splitter choice,
 split sizes and segment ordering are the product code in dist.py."""
 import os
@@ -53,7 +54,75 @@ class CpuOps:
 
     def sort(self, keys, order, key_type):
         out, _ = oracle.sort(keys.numpy(), key_type, descending=bool(order))
-        return torch.from_numpy(out)
+        keys.copy_(torch.from_numpy(out))  # in place, like the device sort
+        return keys
+
+    # fused exchange stand-ins: the "window" is a host tensor and the fused
+    # kernel's peer stores are emulated by a gloo all-to-all that carries the
+    # SENDER's offsets, so the product's offset/capacity logic is what places
+    # every segment
+    def workspace(self, keys, key_type):
+        return None
+
+    def partition_counts(self, keys, spl, order, key_type, ws):
+        return self.partition(keys, spl, order, key_type)[1]
+
+    def window(self, group):
+        return self._win
+
+    def exchange(self, keys, nspl, window, offsets, order, key_type, ws, group=None):
+        world = nspl + 1
+        kb = {"u32": 4, "i32": 4, "u64": 8, "i64": 8}[key_type]
+        if keys is not None and keys.shape[0] > 0:
+            parted, counts = self.partition(keys, self._spl, order, key_type)
+        else:
+            parted, counts = torch.zeros(0, dtype=torch.uint8), torch.zeros(world, dtype=torch.int64)
+        hdr = torch.tensor(list(offsets), dtype=torch.int64)
+        rhdr = torch.empty(world, dtype=torch.int64)
+        dist.all_to_all_single(rhdr, hdr, group=group)
+        rcnt = torch.empty(world, dtype=torch.int64)
+        dist.all_to_all_single(rcnt, counts, group=group)
+        send = parted.contiguous().view(torch.uint8).reshape(-1)
+        recv = torch.empty(int(rcnt.sum()) * kb, dtype=torch.uint8)
+        dist.all_to_all_single(recv, send, output_split_sizes=[int(c) * kb for c in rcnt.tolist()],
+                               input_split_sizes=[int(c) * kb for c in counts.tolist()], group=group)
+        loc = window.local()
+        pos = 0
+        for src in range(world):
+            nb = int(rcnt[src]) * kb
+            o = int(rhdr[src]) * kb
+            loc[o:o + nb] = recv[pos:pos + nb]
+            pos += nb
+
+
+class CpuWindow:
+    def __init__(self):
+        self.buf = torch.zeros(0, dtype=torch.uint8)
+
+    def ensure(self, nbytes, group, device):
+        if nbytes > self.buf.numel():
+            self.buf = torch.zeros(nbytes, dtype=torch.uint8)
+
+    def local(self):
+        return self.buf
+
+
+class CpuOpsFused(CpuOps):
+    """Remembers the splitters the product passes to partition_counts (the
+    fused kernel keeps them in its workspace)."""
+
+    def __init__(self, kt):
+        super().__init__(kt)
+        self._win = CpuWindow()
+
+    def partition_counts(self, keys, spl, order, key_type, ws):
+        self._spl = spl
+        return super().partition_counts(keys, spl, order, key_type, ws)
+
+    def exchange(self, keys, nspl, window, offsets, order, key_type, ws, group=None):
+        if not hasattr(self, "_spl"):
+            self._spl = None
+        return super().exchange(keys, nspl, window, offsets, order, key_type, ws, group)
 
 
 def _free_port():
@@ -84,24 +153,26 @@ def _make(rank, kt, dist_name, n_per):
     return (rng.random(n) ** 4 * 1e9).astype(dt)  # skewed
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, exchange):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     for ci, (kt, desc, dist_name) in enumerate(CASES):
         x = _make(rank, kt, dist_name, 20000)
-        out = dist_sort(torch.from_numpy(x), order=Order(int(desc)), key_type=kt, ops=CpuOps(kt), oversample=16)
+        ops = CpuOpsFused(kt) if exchange == "fused" else CpuOps(kt)
+        out = dist_sort(torch.from_numpy(x), order=Order(int(desc)), key_type=kt, ops=ops, oversample=16,
+                        exchange=exchange)
         q.put((ci, rank, x, out.numpy()))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_dist_sort_gloo(world):
+@pytest.mark.parametrize("world,exchange", [(2, "nccl"), (3, "nccl"), (2, "fused"), (3, "fused")])
+def test_dist_sort_gloo(world, exchange):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, exchange)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -119,3 +190,14 @@ def test_dist_sort_gloo(world):
         if dist_name == "uniform":
             sizes = [len(res[(ci, r)][1]) for r in range(world)]
             assert max(sizes) < 1.5 * (len(allin) / world)  # sampled splitters balance
+
+
+def test_exchange_offsets():
+    from paper_2205_05982_b200.dist import exchange_offsets
+    m = [[3, 1, 0], [2, 5, 4], [0, 7, 1]]  # row s: rank s's counts per destination
+    offs, recv, need = exchange_offsets(m, 1)
+    assert offs == [3, 1, 0] and recv == 13 and need == 13
+    offs, recv, need = exchange_offsets(m, 2)
+    assert offs == [5, 6, 4] and recv == 5
+    offs, recv, _ = exchange_offsets(m, 0)
+    assert offs == [0, 0, 0] and recv == 5

@@ -69,3 +69,60 @@ def test_dist_sort_world1_nccl(cuda):
         assert out.cpu().numpy().tobytes() == np.sort(x).tobytes()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kt,desc,world", [("u64", False, 3), ("i32", True, 4), ("u32", False, 2),
+                                           ("i64", True, 8), ("f32", False, 3), ("k128", False, 3)])
+def test_fused_exchange_virtual_ranks(cuda, kt, desc, world):
+    """vxs_partition_counts + vxs_partition_exchange with `world` ranks
+    emulated in one process (B200_PROFILING: with fewer GPUs than
+    ranks, run the ranks' kernels on one GPU -- none of them waits on
+    another).  Each rank's scatter stores straight into the other ranks'
+    receive buffers at the offsets dist.exchange_offsets computes; the
+    concatenated, locally sorted buffers must equal the oracle's sort."""
+    from paper_2205_05982_b200.dist import choose_splitters, exchange_offsets
+    rng = np.random.default_rng(17 + world)
+    kb = vx.KEY_BYTES[kt]
+    locs = []
+    for r in range(world):
+        n = 300_000 + 7919 * r if r != 1 else 0  # rank 1 holds no keys
+        if kt == "k128":
+            x = rng.integers(0, 2**64, (n, 2), dtype=np.uint64)
+            x[:, 1] >>= 44  # many hi ties
+        elif kt == "f32":
+            x = (rng.standard_normal(n) * 1e3).astype(np.float32)
+        else:
+            dt = {"u32": np.uint32, "i32": np.int32, "u64": np.uint64, "i64": np.int64}[kt]
+            info = np.iinfo(dt)
+            x = rng.integers(info.min, info.max, n, dtype=dt, endpoint=True)
+        locs.append(x)
+    order = vx.Order(int(desc))
+    ktarg = kt if kt == "k128" else None
+    dev = [torch.from_numpy(x).cuda() for x in locs]
+    s = 256 * world
+    smp = [vx.sample(d, s, order=order, seed=r + 1, key_type=ktarg) for r, d in enumerate(dev) if d.shape[0]]
+    words = torch.cat(smp)
+    vx.sort(words, vx.SortConfig(seed=1), key_type={2: "u16", 4: "u32", 8: "u64", 16: "k128"}[kb])
+    spl = choose_splitters(words, world, words.shape[0] // world)
+    ws = [torch.empty(vx.workspace_bytes(max(1, d.shape[0]), kt), dtype=torch.uint8, device="cuda") for d in dev]
+    counts = [vx.partition_counts(d, spl, w, order=order, key_type=ktarg) if d.shape[0]
+              else torch.zeros(world, dtype=torch.int64, device="cuda") for d, w in zip(dev, ws)]
+    m = torch.stack(counts).cpu().tolist()
+    recv = [sum(m[s_][r] for s_ in range(world)) for r in range(world)]
+    bufs = [torch.empty((recv[r], 2) if kb == 16 else (recv[r],), dtype=dev[0].dtype, device="cuda")
+            for r in range(world)]
+    addrs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    for r in range(world):
+        offs, got_recv, _ = exchange_offsets(m, r)
+        assert got_recv == recv[r]
+        if dev[r].shape[0]:
+            vx.partition_exchange(dev[r], world - 1, addrs, torch.tensor(offs, dtype=torch.int64, device="cuda"),
+                                  ws[r], order=order, key_type=ktarg)
+    for b in bufs:
+        if b.shape[0] > 1:
+            vx.sort(b, vx.SortConfig(order=order, seed=1), key_type=ktarg)
+    got = np.concatenate([b.cpu().numpy() for b in bufs])
+    want, _ = oracle.sort(np.concatenate(locs), kt, descending=desc)
+    assert got.tobytes() == want.tobytes()
+    if kt in ("u64", "u32", "i32", "i64"):
+        assert max(recv) < 1.5 * sum(recv) / world  # sampled splitters balance the ranks
