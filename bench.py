@@ -467,7 +467,7 @@ def run_distributed(args):
     src = to_device(x, kt)
     order = vx.Order(int(desc))
     for _ in range(args.warmup):
-        out = dist_sort(src, order=order, key_type=kt)
+        out = dist_sort(src, order=order, key_type=kt, exchange=args.exchange, copy_out=False)
     torch.cuda.synchronize()
     # validation: local sortedness + boundary monotonicity + global count
     ok = check_sorted_device(out, kt, desc)
@@ -483,7 +483,7 @@ def run_distributed(args):
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            out = dist_sort(src, order=order, key_type=kt)
+            out = dist_sort(src, order=order, key_type=kt, exchange=args.exchange, copy_out=False)
             b.record(stream)
             torch.cuda.synchronize()
             times.append(a.elapsed_time(b))
@@ -496,7 +496,7 @@ def run_distributed(args):
     dist.barrier()
     vx.profile_reset()
     vx.profile_enable(True)
-    out = dist_sort(src, order=order, key_type=kt)
+    out = dist_sort(src, order=order, key_type=kt, exchange=args.exchange, copy_out=False)
     torch.cuda.synchronize()
     prof = vx.profile_read()
     vx.profile_enable(False)
@@ -519,7 +519,7 @@ def run_distributed(args):
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
         dev_in.copy_(host, non_blocking=True)
-        res = dist_sort(dev_in, order=order, key_type=kt)
+        res = dist_sort(dev_in, order=order, key_type=kt, exchange=args.exchange, copy_out=False)
         m = min(res.shape[0], host_out.shape[0])
         host_out[:m].copy_(res[:m], non_blocking=True)
         b.record(stream)
@@ -538,7 +538,8 @@ def run_distributed(args):
             "scaling": "weak", "vs_baseline": None, "dtype": kt,
             "data": "synthetic (seeded SplitMix64 per rank; BASELINE.json config shapes)",
             "config": {"workload": args.workload + " (per rank)", "n_per_rank": n, "key_type": kt,
-                       "parallelism": f"distributed sample sort x{world} (NCCL all-gather + all-to-all)"},
+                       "parallelism": f"distributed sample sort x{world} (NCCL all-gather of samples/counts; "
+                                              f"{args.exchange} key exchange)"},
             "validated": bool(int(okt)),
             "gb_per_s_sorted": round(world * n * kb / (ms * 1e-3) / 1e9, 2),
             "clocks": clk.summary(),
@@ -568,6 +569,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-API e2e leg (ncu launch lists only)")
     ap.add_argument("--force-dist", action="store_true", help="run the distributed path even at world size 1 (tests)")
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="distributed key exchange: fused partition+P2P stores (default) or NCCL all-to-all")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
