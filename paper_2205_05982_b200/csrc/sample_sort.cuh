@@ -315,6 +315,12 @@ __device__ __forceinline__ int lower_bound_smem(const W* srt, int lo, int hi, co
   return lo;
 }
 
+// Shared-histogram slot of child c: even children (key ranges; the only
+// ids radix mode produces) fill [0, 256), odd ones (equality buckets)
+// [256, 512), so the hot counters are consecutive words over all 32 banks
+// instead of every other bank.
+__host__ __device__ __forceinline__ int hslot(int c) { return (c >> 1) | ((c & 1) << 8); }
+
 // Children of a bucket with m splitters: ids 0..2m+1 (the last one is the
 // equality bucket of the maximum key, used when the tree pads with it).
 __host__ __device__ __forceinline__ int num_children(int L) { return 2 * ((1 << L) - 1) + 2; }
@@ -752,8 +758,8 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
       const int nc = num_children(L);
       unsigned long long* sg = P.seg + (unsigned long long)(p + blockIdx.x) * kChildStride;
       for (int c = threadIdx.x; c < nc; c += THREADS) {
-        sg[c] = hist[c];
-        hist[c] = 0;
+        sg[c] = hist[hslot(c)];
+        hist[hslot(c)] = 0;
       }
       while (p + 1 < nb && list[p + 1].tile_base <= t) ++p;
       d = list[p];
@@ -780,7 +786,7 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
       if (cnt == TILE && TREE >= 2) {  // radix: stream classify -> count
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i)
-          atomicAdd(&hist[classify_mode<TREE>(enc_x<FLT>(lds_key<W>(kp, i * THREADS + threadIdx.x), X), S)], 1u);
+          atomicAdd(&hist[hslot(classify_mode<TREE>(enc_x<FLT>(lds_key<W>(kp, i * THREADS + threadIdx.x), X), S))], 1u);
       } else if (cnt == TILE) {
         int bk[ITEMS];
 #pragma unroll
@@ -793,11 +799,11 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
         for (int i = 1; i < ITEMS; ++i) same = same && bk[i] == bk[0];
         const int b0 = __shfl_sync(0xffffffffu, bk[0], 0);
         if (__all_sync(0xffffffffu, same && bk[0] == b0)) {
-          if ((threadIdx.x & 31) == 0) atomicAdd(&hist[b0], 32u * ITEMS);
+          if ((threadIdx.x & 31) == 0) atomicAdd(&hist[hslot(b0)], 32u * ITEMS);
         } else {
 #pragma unroll
           for (int i = 0; i < ITEMS; ++i) {  // (wide cells count into a dump slot)
-            atomicAdd(&hist[bk[i] >= 0 ? bk[i] : kChildStride], 1u);
+            atomicAdd(&hist[bk[i] >= 0 ? hslot(bk[i]) : kChildStride], 1u);
             wide |= (bk[i] < 0 ? 1u : 0u) << i;
           }
         }
@@ -807,7 +813,7 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
           const int idx = i * THREADS + threadIdx.x;
           if (idx < cnt) {
             const int b = classify_mode<TREE>(enc_x<FLT>(lds_key<W>(kp, idx), X), S);
-            if (b >= 0) atomicAdd(&hist[b], 1u);
+            if (b >= 0) atomicAdd(&hist[hslot(b)], 1u);
             else wide |= 1u << i;
           }
         }
@@ -829,13 +835,13 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
     while (wide) {
       const int i = __ffs(wide) - 1;
       wide &= wide - 1;
-      atomicAdd(&hist[classify_slow(enc<W>(lds_key<W>(kp, i * THREADS + threadIdx.x), xf), S)], 1u);  // rare
+      atomicAdd(&hist[hslot(classify_slow(enc<W>(lds_key<W>(kp, i * THREADS + threadIdx.x), xf), S))], 1u);  // rare
     }
     __syncthreads();  // stage st fully consumed before it is refilled
   }
   const int nc = num_children(L);
   unsigned long long* sg = P.seg + (unsigned long long)(p + blockIdx.x) * kChildStride;
-  for (int c = threadIdx.x; c < nc; c += THREADS) sg[c] = hist[c];
+  for (int c = threadIdx.x; c < nc; c += THREADS) sg[c] = hist[hslot(c)];
 }
 
 // Column scan of the per-(bucket p, CTA b) child counts written by k_hist:
@@ -1159,17 +1165,17 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     const int b0 = __shfl_sync(0xffffffffu, bk[0], 0);
     if (__all_sync(0xffffffffu, same && bk[0] == b0)) {
       unsigned base = 0;
-      if (lane == 0) base = atomicAdd(&myhist[b0], 32u * ITEMS);
+      if (lane == 0) base = atomicAdd(&myhist[hslot(b0)], 32u * ITEMS);
       base = __shfl_sync(0xffffffffu, base, 0) + lane * ITEMS;
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) bk[i] = (b0 << 16) | (int)(base + i);
     } else if (cnt == TILE) {  // full tile: every id is valid (straight-line code)
 #pragma unroll
-      for (int i = 0; i < ITEMS; ++i) bk[i] = (bk[i] << 16) | (int)atomicAdd(&myhist[bk[i]], 1u);
+      for (int i = 0; i < ITEMS; ++i) bk[i] = (bk[i] << 16) | (int)atomicAdd(&myhist[hslot(bk[i])], 1u);
     } else {
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i)
-        if (bk[i] >= 0) bk[i] = (bk[i] << 16) | (int)atomicAdd(&myhist[bk[i]], 1u);
+        if (bk[i] >= 0) bk[i] = (bk[i] << 16) | (int)atomicAdd(&myhist[hslot(bk[i])], 1u);
     }
     __syncthreads();
     // per child: exclusive prefix across warps, then across children; fold
@@ -1182,7 +1188,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
         const int c = threadIdx.x * PER + j;
         unsigned run = 0;
 #pragma unroll
-        for (int w = 0; w < HC; ++w) run += whist[w * kChildStride + c];
+        for (int w = 0; w < HC; ++w) run += whist[w * kChildStride + hslot(c)];
         tot[j] = run;
         sum += run;
       }
@@ -1198,8 +1204,8 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
         unsigned run = ex;
 #pragma unroll
         for (int w = 0; w < HC; ++w) {
-          const unsigned v = whist[w * kChildStride + c];
-          whist[w * kChildStride + c] = run;
+          const unsigned v = whist[w * kChildStride + hslot(c)];
+          whist[w * kChildStride + hslot(c)] = run;
           run += v;
         }
         gres[j] = 0;
@@ -1214,17 +1220,17 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       W* staged = reinterpret_cast<W*>(stage);
       if (radix && cnt == TILE) {  // child ids are recomputed from the keys at write-out
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) staged[myhist[bk[i] >> 16] + (unsigned)(bk[i] & 0xFFFF)] = k[i];
+        for (int i = 0; i < ITEMS; ++i) staged[myhist[hslot(bk[i] >> 16)] + (unsigned)(bk[i] & 0xFFFF)] = k[i];
       } else if (radix) {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-          if (bk[i] >= 0) staged[myhist[bk[i] >> 16] + (unsigned)(bk[i] & 0xFFFF)] = k[i];
+          if (bk[i] >= 0) staged[myhist[hslot(bk[i] >> 16)] + (unsigned)(bk[i] & 0xFFFF)] = k[i];
         }
       } else if (cnt == TILE) {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
           const int c = bk[i] >> 16;
-          const unsigned pos = myhist[c] + (unsigned)(bk[i] & 0xFFFF);
+          const unsigned pos = myhist[hslot(c)] + (unsigned)(bk[i] & 0xFFFF);
           staged[pos] = k[i];
           stage_b[pos] = (unsigned short)c;
         }
@@ -1233,7 +1239,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
         for (int i = 0; i < ITEMS; ++i) {
           if (bk[i] >= 0) {
             const int c = bk[i] >> 16;
-            const unsigned pos = myhist[c] + (unsigned)(bk[i] & 0xFFFF);
+            const unsigned pos = myhist[hslot(c)] + (unsigned)(bk[i] & 0xFFFF);
             staged[pos] = k[i];
             stage_b[pos] = (unsigned short)c;
           }
