@@ -163,9 +163,9 @@ __device__ __forceinline__ void block_sort(W (&k)[ITEMS], W* smem) {
 //   1. block min/max, then one returning shared atomic per key (bin count and
 //      the key's rank inside its bin); sum(2*rank + 1) = sum(count^2) and
 //      max(rank) + 1 = the largest bin, both reduced over the block;
-//   2. exclusive scan of the bin counts -- thread t owns BPT consecutive
-//      counters in 16-byte groups padded so LDS.128/STS.128 are
-//      conflict-free;
+//   2. exclusive scan of the bin counts (16-bit, two per word) -- thread t
+//      owns BPT consecutive bins in 16-byte groups padded so LDS.128/STS.128
+//      are conflict-free;
 //   3. keys scattered to smem grouped by bin (padding keys fill [size, TOTAL));
 //   4. each thread takes ITEMS consecutive positions into registers and the
 //      warp runs C rounds of odd-even transposition sort, C = largest bin:
@@ -184,14 +184,28 @@ struct BinSort {
   static constexpr int kNB = kTotal <= 4096 ? 2 * kTotal : kTotal;
   static constexpr int kBPT = kNB / THREADS;  // bins per thread in the scan
   static constexpr int kNBBits = kNB == 512 ? 9 : kNB == 1024 ? 10 : kNB == 2048 ? 11 : kNB == 4096 ? 12 : kNB == 8192 ? 13 : 14;
-  static constexpr int kEnd = kNB + kNB / 8;  // padded slot of bin NB (end sentinel)
-  static constexpr int kDummy = kEnd + 1;     // slot of bin NB + 1 (padding keys)
+  // 8/16-byte keys: bin counters are 16-bit halves packed two per word (bin
+  // b: word b/2, half b&1), half the smem of 32-bit counters for the zero
+  // fill, the scan and its write-back (counts and prefixes are < 2^16).
+  // <= 4-byte keys keep one 32-bit counter per bin: their kernel is issue-
+  // bound, and neighbouring bins sharing a word serialise their atomics.
+  static constexpr bool kPacked = sizeof(W) >= 8;
+  static constexpr int kBinsPerWord = kPacked ? 2 : 1;
+  static constexpr int kWords = kNB / kBinsPerWord;
+  static constexpr int kWPT = kBPT / kBinsPerWord;  // words per thread in the scan
+  static constexpr int kEnd = kWords + kWords / 8;  // padded word of bin NB (end sentinel, low half)
+  static constexpr int kDummy = kEnd + 1;           // word of bin NB + kBinsPerWord (padding keys, low half)
   static constexpr int kCnt = (kDummy + 4) & ~3;
   static constexpr int kMaxBin = 64;
   static constexpr size_t kSmem = (size_t)kTotal * sizeof(W) + (size_t)kCnt * 4;
-  static_assert((1 << kNBBits) == kNB && kBPT % 4 == 0 && kBPT <= 32, "bin count");
-  // 4 pad words after every 32 counters: thread t's group starts at bank 4t
-  __host__ __device__ static __forceinline__ int slot(int b) { return b + ((b >> 3) & ~3); }
+  static_assert((1 << kNBBits) == kNB && kWPT % 4 == 0 && kBPT <= 32, "bin count");
+  // 4 pad words after every 32 counter words: the 16-byte groups of 8
+  // threads in one LDS.128 phase land on distinct banks
+  __host__ __device__ static __forceinline__ int wslot(int w) { return w + ((w >> 3) & ~3); }
+  __device__ static __forceinline__ unsigned half(const unsigned* cnt, int b) {
+    if constexpr (kPacked) return (cnt[wslot(b >> 1)] >> ((b & 1) << 4)) & 0xFFFFu;
+    else return cnt[wslot(b)];
+  }
   // smem position of key p: the 16-byte chunks of row r = p / ITEMS are
   // XOR-swizzled by r & 7 so the per-thread row loads/stores (LDS.128 /
   // STS.128, rows 64-256 B apart) are conflict-free.  Each chunk bit is
@@ -327,26 +341,39 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
   block_minmax<W, THREADS, ITEMS>(k, lo, hi, red_lo, red_hi);  // (its barrier covers cnt)
   const int bl = key_bitlen(key_sub(hi, lo));
   const int shift = bl > BS::kNBBits ? bl - BS::kNBBits : 0;
-  unsigned br[ITEMS];  // padded counter slot << 16 | rank inside the bin
+  unsigned br[ITEMS];  // counter word << 17 | half << 16 | rank inside the bin
   unsigned sq = 0;     // sum over keys of 2*rank + 1 = sum over bins of count^2
   unsigned mx = 0;     // largest rank
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const bool valid = i * THREADS + tid < size;
-    const int sl = valid ? BS::slot((int)key_shr32(key_sub(k[i], lo), shift)) : BS::kDummy;
-    const unsigned r = atomicAdd(&cnt[sl], 1u);
-    br[i] = ((unsigned)sl << 16) | r;
+    const unsigned b = valid ? key_shr32(key_sub(k[i], lo), shift) : (unsigned)(NB + BS::kBinsPerWord);
+    unsigned r;
+    if constexpr (BS::kPacked) {
+      const int w = BS::wslot((int)(b >> 1));
+      const unsigned h = (b & 1u) << 4;
+      r = (atomicAdd(&cnt[w], 1u << h) >> h) & 0xFFFFu;
+      br[i] = ((unsigned)w << 17) | ((b & 1u) << 16) | r;
+    } else {
+      const int w = BS::wslot((int)b);
+      r = atomicAdd(&cnt[w], 1u);
+      br[i] = ((unsigned)w << 17) | r;
+    }
     sq += 2u * r + 1u;
     mx = valid ? umax(mx, r) : mx;
   }
   __syncthreads();
   // exclusive scan over the bins; thread t owns bins [t*BPT, (t+1)*BPT)
-  uint4* cg = reinterpret_cast<uint4*>(cnt + BS::slot(tid * BPT));
+  uint4* cg = reinterpret_cast<uint4*>(cnt + BS::wslot(tid * BS::kWPT));
   unsigned sum = 0;
 #pragma unroll
-  for (int j = 0; j < BPT / 4; ++j) {
+  for (int j = 0; j < BS::kWPT / 4; ++j) {
     const uint4 c = cg[j];
-    sum += c.x + c.y + c.z + c.w;
+    if constexpr (BS::kPacked)
+      sum += (c.x & 0xFFFFu) + (c.x >> 16) + (c.y & 0xFFFFu) + (c.y >> 16) + (c.z & 0xFFFFu) + (c.z >> 16) +
+             (c.w & 0xFFFFu) + (c.w >> 16);
+    else
+      sum += c.x + c.y + c.z + c.w;
   }
   unsigned incl = sum;
 #pragma unroll
@@ -376,12 +403,26 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
   // block-uniform rejection; cnt is no longer read
   const unsigned pad = (unsigned)(TOTAL - size);  // the dummy bin adds pad^2
   if (tsq - pad * pad > 4u * (unsigned)size + 256u || rounds > (unsigned)BS::kMaxBin) return false;
+  auto pre = [&](unsigned x) {  // count(s) -> exclusive prefix(es), same packing
+    if constexpr (BS::kPacked) {
+      const unsigned l = base, h = base + (x & 0xFFFFu);
+      base = h + (x >> 16);
+      return l | (h << 16);
+    } else {
+      const unsigned l = base;
+      base += x;
+      return l;
+    }
+  };
 #pragma unroll
-  for (int j = 0; j < BPT / 4; ++j) {  // (only this thread touches these counters)
-    uint4 c = cg[j];
-    const unsigned x = base, y = x + c.x, z = y + c.y, w = z + c.z;
-    base = w + c.w;
-    cg[j] = make_uint4(x, y, z, w);
+  for (int j = 0; j < BS::kWPT / 4; ++j) {  // (only this thread touches these counters)
+    const uint4 c = cg[j];
+    uint4 o;
+    o.x = pre(c.x);
+    o.y = pre(c.y);
+    o.z = pre(c.z);
+    o.w = pre(c.w);
+    cg[j] = o;
   }
   if (tid == THREADS - 1) {
     cnt[BS::kEnd] = (unsigned)size;
@@ -389,8 +430,10 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
   }
   __syncthreads();
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i)
-    sk[BS::swz((int)(cnt[br[i] >> 16] + (br[i] & 0xFFFFu)))] = i * THREADS + tid < size ? k[i] : key_max<W>();
+  for (int i = 0; i < ITEMS; ++i) {
+    const unsigned s0 = BS::kPacked ? (cnt[br[i] >> 17] >> (((br[i] >> 16) & 1u) << 4)) & 0xFFFFu : cnt[br[i] >> 17];
+    sk[BS::swz((int)(s0 + (br[i] & 0xFFFFu)))] = i * THREADS + tid < size ? k[i] : key_max<W>();
+  }
   __syncthreads();
   // odd-even transposition rounds over this thread's row of ITEMS positions
   W v[ITEMS];
@@ -429,7 +472,7 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
     const int p = warp * 32 * ITEMS;
     if (p < size) {
       const int b = (int)key_shr32(key_sub(sk[BS::swz(p)], lo), shift);
-      const int s = (int)cnt[BS::slot(b)], e = (int)cnt[BS::slot(b + 1)];
+      const int s = (int)BS::half(cnt, b), e = (int)BS::half(cnt, b + 1);
       if (s < p) {
         for (int a = s + 1; a < e; ++a) {
           const W x = sk[BS::swz(a)];
