@@ -87,3 +87,24 @@ def test_uniform_items_many_sizes(cuda):
         for n in list(range(257, 8193, 479)):
             x = rand_keys(kt, n, rng)
             check(x, kt, bool(n & 1))
+
+
+@pytest.mark.parametrize("kt", ["u64", "i64", "f64", "k128"])
+def test_item_straddling_high_word(cuda, kt):
+    """64-bit items whose keys cross a 2^32 (high-word) boundary with a tiny
+    range: the high-word bounds are coarse (the item is rejected and sorted by
+    the fallback) and still exact; also items inside one high word."""
+    rng = np.random.default_rng(16)
+    for n, base in ((3000, 2**32 - 1500), (8000, 7 * 2**32 - 10), (2048, 5 * 2**32 + 1000),
+                    (200_000, 2**40 - 100_000)):
+        v = (base + rng.integers(0, 3000 if n < 100_000 else 200_000, n)).astype(np.uint64)
+        if kt == "k128":
+            x = np.zeros((n, 2), dtype=np.uint64)
+            x[:, 0] = v
+            x[:, 1] = rng.integers(0, 3, n).astype(np.uint64)
+        elif kt == "f64":
+            x = v.astype(np.float64)
+        else:
+            x = v.view(np.int64) if kt == "i64" else v
+        for desc in (False, True):
+            check(x, kt, desc)
