@@ -295,6 +295,35 @@ __global__ void k_ctrl_out(const Ctrl* c, Ctrl* out) {
   __threadfence_system();
 }
 
+// Per (thread, device) side stream + fork/join events for the base-case
+// classes (run_sort).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+struct SideStreams {
+  std::unordered_map<int, SideStream> m;
+  ~SideStreams() {
+    for (auto& kv : m) {
+      cudaEventDestroy(kv.second.fork);
+      cudaEventDestroy(kv.second.join);
+      cudaStreamDestroy(kv.second.s);
+    }
+  }
+};
+SideStream* side_stream() {
+  thread_local SideStreams ts;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto it = ts.m.find(dev);
+  if (it != ts.m.end()) return &it->second;
+  SideStream x;
+  if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+  return &(ts.m[dev] = x);
+}
+
 struct CtrlMirror {
   std::unordered_map<int, Ctrl*> buf;
   ~CtrlMirror() {
@@ -391,12 +420,50 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
     if (rs != VXS_OK) return rs;
     ++launches;
   }
-  if (h.item_count[0]) { launch_final<W, 0>(P, h.item_count[0], st); ++launches; }
-  if (h.item_count[1]) { launch_final<W, 1>(P, h.item_count[1], st); ++launches; }
-  if (h.item_count[2]) { launch_final<W, 2>(P, h.item_count[2], st); ++launches; }
-  if (h.item_count[3]) { launch_final<W, 3>(P, h.item_count[3], st); ++launches; }
-  if constexpr (Cfg<W>::kCap >= 8192) {
-    if (h.item_count[4]) { launch_final<W, 4>(P, h.item_count[4], st); ++launches; }
+  // The size classes and the equality-bucket copy touch disjoint items: the
+  // class holding the most keys runs on the caller's stream, the rest on a
+  // side stream underneath it (forked and joined with events, no host sync);
+  // the fallback for rejected items follows the join.
+  {
+    constexpr unsigned long long kClassCap[5] = {256, 1024, 2048, 4096, 8192};
+    int main_cls = 0;
+    for (int c = 1; c < kNumSortClasses; ++c)
+      if (h.item_count[c] * kClassCap[c] > h.item_count[main_cls] * kClassCap[main_cls]) main_cls = c;
+    const bool copy = h.item_count[kListCopySmall] || h.item_count[kListCopyBig];
+    int others = copy ? 1 : 0;
+    for (int c = 0; c < kNumSortClasses; ++c) others += (c != main_cls && h.item_count[c]) ? 1 : 0;
+    SideStream* ss = others ? side_stream() : nullptr;
+    cudaStream_t sd = ss ? ss->s : st;
+    if (ss) {
+      VXS_CK(cudaEventRecord(ss->fork, st), "fork");
+      VXS_CK(cudaStreamWaitEvent(sd, ss->fork, 0), "fork wait");
+    }
+    auto launch_cls = [&](int c, cudaStream_t s2) {
+      switch (c) {
+        case 0: launch_final<W, 0>(P, h.item_count[0], s2); break;
+        case 1: launch_final<W, 1>(P, h.item_count[1], s2); break;
+        case 2: launch_final<W, 2>(P, h.item_count[2], s2); break;
+        case 3: launch_final<W, 3>(P, h.item_count[3], s2); break;
+        default:
+          if constexpr (Cfg<W>::kCap >= 8192) launch_final<W, 4>(P, h.item_count[4], s2);
+          break;
+      }
+      ++launches;
+    };
+    for (int c = 0; c < kNumSortClasses; ++c)
+      if (c != main_cls && h.item_count[c]) launch_cls(c, sd);
+    if (copy) {
+      ProfScope ps(K_COPY, sd);
+      auto fn = k_copy<W>;
+      const int g = grid_for((const void*)fn, 256, 0);
+      fn<<<g, 256, 0, sd>>>(P);
+      ++launches;
+    }
+    if (h.item_count[main_cls]) launch_cls(main_cls, st);
+    if (ss) {
+      VXS_CK(cudaEventRecord(ss->join, sd), "join");
+      VXS_CK(cudaStreamWaitEvent(st, ss->join, 0), "join wait");
+    }
   }
   {
     // items rejected by the counting-sort base case (count lives on the device)
@@ -409,13 +476,6 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
       fn<<<g, SortClass<4>::T, smem, st>>>(P);
       ++launches;
     }
-  }
-  if (h.item_count[kListCopySmall] || h.item_count[kListCopyBig]) {
-    ProfScope ps(K_COPY, st);
-    auto fn = k_copy<W>;
-    const int g = grid_for((const void*)fn, 256, 0);
-    fn<<<g, 256, 0, st>>>(P);
-    ++launches;
   }
   VXS_CK(cudaGetLastError(), "final launch");
   if (owned) VXS_CK(cudaFreeAsync(owned, st), "workspace free");
