@@ -887,6 +887,55 @@ __global__ void __launch_bounds__(128) k_segscan(Params<W> P) {
   }
 }
 
+// k_segscan for the root level (one bucket, every CTA of the grid holds a
+// row): one CTA per 32-child chunk, its 32 warps split the rows (one
+// round trip of loads instead of a serial walk down ~300 rows per lane).
+template <typename W>
+__global__ void __launch_bounds__(1024) k_segscan_root(Params<W> P) {
+  __shared__ unsigned long long part[32][33];
+  const unsigned long long packed = P.ctrl->split_packed[P.cur];
+  if ((int)(packed >> 40) == 0) return;
+  const unsigned long long T = packed & kTileMask;
+  const unsigned long long tpc = (T + P.grid - 1) / P.grid;
+  const SplitDesc d = P.split[P.cur][0];
+  const int nc = num_children((int)(d.L & 0xFFu));
+  const int rows = (int)((ntiles_dev<W>(d.size) + tpc - 1) / tpc);  // CTAs b = 0 .. rows-1
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int per = (rows + 31) / 32;
+  constexpr int R = 16;
+  for (int c0 = blockIdx.x * 32; c0 < nc; c0 += gridDim.x * 32) {
+    const int c = c0 + lane;
+    const int r0 = warp * per, r1 = r0 + per < rows ? r0 + per : rows;
+    unsigned long long sum = 0;
+    for (int r = r0; r < r1; r += R) {
+      unsigned long long v[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) v[j] = (r + j < r1 && c < nc) ? P.seg[(unsigned long long)(r + j) * kChildStride + c] : 0ull;
+#pragma unroll
+      for (int j = 0; j < R; ++j) sum += v[j];
+    }
+    part[warp][lane] = sum;
+    __syncthreads();
+    unsigned long long run = 0, tot = 0;
+    for (int w = 0; w < 32; ++w) {
+      run += w < warp ? part[w][lane] : 0ull;
+      tot += part[w][lane];
+    }
+    for (int r = r0; r < r1; r += R) {
+      unsigned long long v[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) v[j] = (r + j < r1 && c < nc) ? P.seg[(unsigned long long)(r + j) * kChildStride + c] : 0ull;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        if (r + j < r1 && c < nc) P.seg[(unsigned long long)(r + j) * kChildStride + c] = run;
+        run += v[j];
+      }
+    }
+    if (warp == 0 && c < nc) P.counts[c] = tot;
+    __syncthreads();
+  }
+}
+
 // Per split bucket: child offsets -> cursors; children become next-level
 // split buckets, base-case items (grouping adjacent small children into one
 // item of <= Cap keys) or copy items (equality buckets).

@@ -253,9 +253,13 @@ vxs_status launch_level(Params<W>& P, cudaStream_t st, int& launches) {
   }
   {
     ProfScope ps(K_SEGSCAN + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
-    auto fn = k_segscan<W>;
-    const int g = grid_for((const void*)fn, 128, 0);
-    fn<<<g, 128, 0, st>>>(P);
+    if (P.level == 0) {  // the root bucket: every CTA holds a row
+      k_segscan_root<W><<<(kChildStride + 31) / 32, 1024, 0, st>>>(P);
+    } else {
+      auto fn = k_segscan<W>;
+      const int g = grid_for((const void*)fn, 128, 0);
+      fn<<<g, 128, 0, st>>>(P);
+    }
   }
   {
     ProfScope ps(K_PLAN + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
@@ -1412,7 +1416,7 @@ vxs_status vxs_partition(const void* d_keys, size_t n, vxs_key_type type, vxs_or
       auto fn = k_hist<W>;
       fn<<<P.grid, Cfg<W>::kHistThreads, hist_smem<W>(), st>>>(P);
     }
-    k_segscan<W><<<16, 128, 0, st>>>(P);
+    k_segscan_root<W><<<(kChildStride + 31) / 32, 1024, 0, st>>>(P);
     k_plan<W><<<1, kChildStride, 0, st>>>(P);
     {
       auto fn = k_scatter<W>;
@@ -1453,7 +1457,7 @@ vxs_status vxs_partition_counts(const void* d_keys, size_t n, vxs_key_type type,
     k_init<W><<<1, 32, 0, st>>>(P);
     k_part_setup<W><<<1, 256, 0, st>>>(P, static_cast<const W*>(d_splitters), nspl, L);
     k_hist<W><<<P.grid, Cfg<W>::kHistThreads, hist_smem<W>(), st>>>(P);
-    k_segscan<W><<<16, 128, 0, st>>>(P);
+    k_segscan_root<W><<<(kChildStride + 31) / 32, 1024, 0, st>>>(P);
     k_plan<W><<<1, kChildStride, 0, st>>>(P);
     k_part_counts<W><<<1, 256, 0, st>>>(P, nseg, reinterpret_cast<unsigned long long*>(d_seg_counts));
     VXS_CK(cudaGetLastError(), "partition_counts");
