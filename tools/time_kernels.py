@@ -42,6 +42,16 @@ for _ in range(2):
     buf.copy_(src)
     run_op()
 torch.cuda.synchronize()
+plain = []
+for _ in range(a.reps):  # unprofiled (no per-launch events)
+    buf.copy_(src)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    run_op()
+    e.record()
+    torch.cuda.synchronize()
+    plain.append(s.elapsed_time(e))
 vx.profile_reset()
 vx.profile_enable(True)
 ev = []
@@ -55,5 +65,5 @@ for _ in range(a.reps):
     torch.cuda.synchronize()
     ev.append(s.elapsed_time(e))
 prof = vx.profile_read()
-print(a.workload, a.op, "ms/op", round(sum(ev) / len(ev), 4),
+print(a.workload, a.op, "ms/op", round(sum(plain) / len(plain), 4), "profiled", round(sum(ev) / len(ev), 4),
       {k: round(v[1] / a.reps, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])})
