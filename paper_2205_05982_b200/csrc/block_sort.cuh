@@ -14,6 +14,10 @@
 #pragma once
 #include "keys.cuh"
 
+#ifndef VXS_TWOPASS_U64  // build-time experiment switch (A/B timing); product: 0
+#define VXS_TWOPASS_U64 0
+#endif
+
 namespace vxs {
 
 // In-register bitonic sort of N (power of two) keys, ascending.
@@ -160,13 +164,15 @@ __device__ __forceinline__ void block_sort(W (&k)[ITEMS], W* smem) {
 // [lo, hi]: the level above split by radix digit or by sample quantiles.  So
 // the base case is a counting sort on NB = 2*TOTAL linear bins of
 // (key - lo) >> shift, shift = bitlen(hi - lo) - log2 NB:
-//   1. block min/max, then one returning shared atomic per key (bin count and
-//      the key's rank inside its bin); sum(2*rank + 1) = sum(count^2) and
-//      max(rank) + 1 = the largest bin, both reduced over the block;
+//   1. block min/max, then one fire-and-forget shared atomic per key (bin
+//      counts);
 //   2. exclusive scan of the bin counts (16-bit, two per word) -- thread t
 //      owns BPT consecutive bins in 16-byte groups padded so LDS.128/STS.128
 //      are conflict-free;
-//   3. keys scattered to smem grouped by bin (padding keys fill [size, TOTAL));
+//      the same pass reduces sum(count^2) and the largest bin;
+//   3. keys scattered to smem grouped by bin, each taking the next slot of
+//      its bin with a returning atomic on the prefix (padding keys fill
+//      [size, TOTAL));
 //   4. each thread takes ITEMS consecutive positions into registers and the
 //      warp runs C rounds of odd-even transposition sort, C = largest bin:
 //      pairs from different bins are already ordered and never swap, so C
@@ -190,6 +196,10 @@ struct BinSort {
   // <= 4-byte keys keep one 32-bit counter per bin: their kernel is issue-
   // bound, and neighbouring bins sharing a word serialise their atomics.
   static constexpr bool kPacked = sizeof(W) >= 8;
+  // ranks: 8-byte keys rank in the counting pass (one returning atomic per
+  // key, measured best for them); the others count fire-and-forget and take
+  // positions with a returning atomic on the prefixes in the scatter pass
+  static constexpr bool kTwoPass = sizeof(W) != 8 || VXS_TWOPASS_U64;
   static constexpr int kBinsPerWord = kPacked ? 2 : 1;
   static constexpr int kWords = kNB / kBinsPerWord;
   static constexpr int kWPT = kBPT / kBinsPerWord;  // words per thread in the scan
@@ -341,39 +351,54 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
   block_minmax<W, THREADS, ITEMS>(k, lo, hi, red_lo, red_hi);  // (its barrier covers cnt)
   const int bl = key_bitlen(key_sub(hi, lo));
   const int shift = bl > BS::kNBBits ? bl - BS::kNBBits : 0;
-  unsigned br[ITEMS];  // counter word << 17 | half << 16 | rank inside the bin
-  unsigned sq = 0;     // sum over keys of 2*rank + 1 = sum over bins of count^2
-  unsigned mx = 0;     // largest rank
+  // pass 1: count; kTwoPass: fire-and-forget shared atomics, else a
+  // returning atomic that also yields the key's rank inside its bin
+  unsigned br[ITEMS];  // counter word << 17 | half << 16 [| rank]
+  unsigned sq = 0, mx = 0;  // !kTwoPass: sum of 2*rank + 1 (= sum count^2), max rank
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const bool valid = i * THREADS + tid < size;
     const unsigned b = valid ? key_shr32(key_sub(k[i], lo), shift) : (unsigned)(NB + BS::kBinsPerWord);
-    unsigned r;
-    if constexpr (BS::kPacked) {
-      const int w = BS::wslot((int)(b >> 1));
-      const unsigned h = (b & 1u) << 4;
-      r = (atomicAdd(&cnt[w], 1u << h) >> h) & 0xFFFFu;
-      br[i] = ((unsigned)w << 17) | ((b & 1u) << 16) | r;
+    const int w = BS::kPacked ? BS::wslot((int)(b >> 1)) : BS::wslot((int)b);
+    const unsigned h = BS::kPacked ? (b & 1u) << 4 : 0u;
+    br[i] = ((unsigned)w << 17) | ((h >> 4) << 16);
+    if constexpr (BS::kTwoPass) {
+      atomicAdd(&cnt[w], 1u << h);
     } else {
-      const int w = BS::wslot((int)b);
-      r = atomicAdd(&cnt[w], 1u);
-      br[i] = ((unsigned)w << 17) | r;
+      const unsigned r = (atomicAdd(&cnt[w], 1u << h) >> h) & 0xFFFFu;
+      br[i] |= r;
+      sq += 2u * r + 1u;
+      mx = valid ? umax(mx, r + 1u) : mx;
     }
-    sq += 2u * r + 1u;
-    mx = valid ? umax(mx, r) : mx;
   }
   __syncthreads();
   // exclusive scan over the bins; thread t owns bins [t*BPT, (t+1)*BPT)
+  // (kTwoPass: sum(count^2), the cost of the rounds, and the largest bin too)
   uint4* cg = reinterpret_cast<uint4*>(cnt + BS::wslot(tid * BS::kWPT));
   unsigned sum = 0;
+  auto acc = [&](unsigned x) {
+    if constexpr (BS::kPacked) {
+      const unsigned l = x & 0xFFFFu, hh = x >> 16;
+      sum += l + hh;
+      if constexpr (BS::kTwoPass) {
+        sq += l * l + hh * hh;
+        mx = umax(mx, umax(l, hh));
+      }
+    } else {
+      sum += x;
+      if constexpr (BS::kTwoPass) {
+        sq += x * x;
+        mx = umax(mx, x);
+      }
+    }
+  };
 #pragma unroll
   for (int j = 0; j < BS::kWPT / 4; ++j) {
     const uint4 c = cg[j];
-    if constexpr (BS::kPacked)
-      sum += (c.x & 0xFFFFu) + (c.x >> 16) + (c.y & 0xFFFFu) + (c.y >> 16) + (c.z & 0xFFFFu) + (c.z >> 16) +
-             (c.w & 0xFFFFu) + (c.w >> 16);
-    else
-      sum += c.x + c.y + c.z + c.w;
+    acc(c.x);
+    acc(c.y);
+    acc(c.z);
+    acc(c.w);
   }
   unsigned incl = sum;
 #pragma unroll
@@ -397,17 +422,19 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
   for (int w = 0; w < NW; ++w) {
     base += w < warp ? s_tot[w] : 0u;
     tsq += s_sq[w];
-    rounds = umax(rounds, s_mx[w]);
+    rounds = umax(rounds, s_mx[w]);  // largest bin
   }
-  rounds += 1;  // largest bin
+  if constexpr (!BS::kTwoPass) {
+    const unsigned pad = (unsigned)(TOTAL - size);  // the dummy bin added pad^2
+    tsq -= pad * pad;
+  }
   // block-uniform rejection; cnt is no longer read
-  const unsigned pad = (unsigned)(TOTAL - size);  // the dummy bin adds pad^2
-  if (tsq - pad * pad > 4u * (unsigned)size + 256u || rounds > (unsigned)BS::kMaxBin) return false;
+  if (tsq > 4u * (unsigned)size + 256u || rounds > (unsigned)BS::kMaxBin) return false;
   auto pre = [&](unsigned x) {  // count(s) -> exclusive prefix(es), same packing
     if constexpr (BS::kPacked) {
-      const unsigned l = base, h = base + (x & 0xFFFFu);
-      base = h + (x >> 16);
-      return l | (h << 16);
+      const unsigned l = base, hh = base + (x & 0xFFFFu);
+      base = hh + (x >> 16);
+      return l | (hh << 16);
     } else {
       const unsigned l = base;
       base += x;
@@ -429,10 +456,16 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
     cnt[BS::kDummy] = (unsigned)size;  // padding keys go to [size, TOTAL)
   }
   __syncthreads();
+  // pass 2: scatter grouped by bin.  kTwoPass: each key takes the next slot
+  // of its bin (returning atomic on the prefix; afterwards cnt[b] holds the
+  // END of bin b); else prefix + rank (cnt keeps the bin starts)
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
-    const unsigned s0 = BS::kPacked ? (cnt[br[i] >> 17] >> (((br[i] >> 16) & 1u) << 4)) & 0xFFFFu : cnt[br[i] >> 17];
-    sk[BS::swz((int)(s0 + (br[i] & 0xFFFFu)))] = i * THREADS + tid < size ? k[i] : key_max<W>();
+    const unsigned h = ((br[i] >> 16) & 1u) << 4;
+    unsigned pos;
+    if constexpr (BS::kTwoPass) pos = (atomicAdd(&cnt[br[i] >> 17], 1u << h) >> h) & 0xFFFFu;
+    else pos = ((cnt[br[i] >> 17] >> h) & 0xFFFFu) + (br[i] & 0xFFFFu);
+    sk[BS::swz((int)pos)] = i * THREADS + tid < size ? k[i] : key_max<W>();
   }
   __syncthreads();
   // odd-even transposition rounds over this thread's row of ITEMS positions
@@ -472,7 +505,9 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
     const int p = warp * 32 * ITEMS;
     if (p < size) {
       const int b = (int)key_shr32(key_sub(sk[BS::swz(p)], lo), shift);
-      const int s = (int)BS::half(cnt, b), e = (int)BS::half(cnt, b + 1);
+      // (kTwoPass: after pass 2 cnt holds bin ENDS, bin b is [end(b-1), end(b)))
+      const int s = BS::kTwoPass ? (b > 0 ? (int)BS::half(cnt, b - 1) : 0) : (int)BS::half(cnt, b);
+      const int e = BS::kTwoPass ? (int)BS::half(cnt, b) : (int)BS::half(cnt, b + 1);
       if (s < p) {
         for (int a = s + 1; a < e; ++a) {
           const W x = sk[BS::swz(a)];
