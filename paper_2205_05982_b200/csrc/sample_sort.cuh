@@ -1207,24 +1207,23 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       for (int i = 0; i < ITEMS; ++i)
         if (bk[i] == -1) bk[i] = classify_slow(k[i], S);
     }
-    // rank within (warp, child); bk[] becomes child << 16 | rank
+    // count per child (fire-and-forget shared atomics; positions are taken in
+    // the staging pass with returning atomics on the prefixes); a warp whose
+    // whole sub-tile is one child counts (and later reserves) with one atomic
     bool same = bk[0] >= 0;
 #pragma unroll
     for (int i = 1; i < ITEMS; ++i) same = same && bk[i] == bk[0];
     const int b0 = __shfl_sync(0xffffffffu, bk[0], 0);
-    if (__all_sync(0xffffffffu, same && bk[0] == b0)) {
-      unsigned base = 0;
-      if (lane == 0) base = atomicAdd(&myhist[hslot(b0)], 32u * ITEMS);
-      base = __shfl_sync(0xffffffffu, base, 0) + lane * ITEMS;
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) bk[i] = (b0 << 16) | (int)(base + i);
+    const bool uni = __all_sync(0xffffffffu, same && bk[0] == b0);
+    if (uni) {
+      if (lane == 0) atomicAdd(&myhist[hslot(b0)], 32u * ITEMS);
     } else if (cnt == TILE) {  // full tile: every id is valid (straight-line code)
 #pragma unroll
-      for (int i = 0; i < ITEMS; ++i) bk[i] = (bk[i] << 16) | (int)atomicAdd(&myhist[hslot(bk[i])], 1u);
+      for (int i = 0; i < ITEMS; ++i) atomicAdd(&myhist[hslot(bk[i])], 1u);
     } else {
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i)
-        if (bk[i] >= 0) bk[i] = (bk[i] << 16) | (int)atomicAdd(&myhist[hslot(bk[i])], 1u);
+        if (bk[i] >= 0) atomicAdd(&myhist[hslot(bk[i])], 1u);
     }
     __syncthreads();
     // per child: exclusive prefix across warps, then across children; fold
@@ -1267,30 +1266,39 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       }
       __syncthreads();
       W* staged = reinterpret_cast<W*>(stage);
-      if (radix && cnt == TILE) {  // child ids are recomputed from the keys at write-out
+      // stage grouped by child: each key takes the next slot of its child
+      // (returning shared atomic on the child's prefix)
+      if (uni) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(&myhist[hslot(b0)], 32u * ITEMS);
+        base = __shfl_sync(0xffffffffu, base, 0) + lane * ITEMS;
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) staged[myhist[hslot(bk[i] >> 16)] + (unsigned)(bk[i] & 0xFFFF)] = k[i];
+        for (int i = 0; i < ITEMS; ++i) {
+          staged[base + i] = k[i];
+          if (!radix) stage_b[base + i] = (unsigned short)b0;
+        }
+      } else if (radix && cnt == TILE) {  // child ids are recomputed from the keys at write-out
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) staged[atomicAdd(&myhist[hslot(bk[i])], 1u)] = k[i];
       } else if (radix) {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-          if (bk[i] >= 0) staged[myhist[hslot(bk[i] >> 16)] + (unsigned)(bk[i] & 0xFFFF)] = k[i];
+          if (bk[i] >= 0) staged[atomicAdd(&myhist[hslot(bk[i])], 1u)] = k[i];
         }
       } else if (cnt == TILE) {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-          const int c = bk[i] >> 16;
-          const unsigned pos = myhist[hslot(c)] + (unsigned)(bk[i] & 0xFFFF);
+          const unsigned pos = atomicAdd(&myhist[hslot(bk[i])], 1u);
           staged[pos] = k[i];
-          stage_b[pos] = (unsigned short)c;
+          stage_b[pos] = (unsigned short)bk[i];
         }
       } else {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
           if (bk[i] >= 0) {
-            const int c = bk[i] >> 16;
-            const unsigned pos = myhist[hslot(c)] + (unsigned)(bk[i] & 0xFFFF);
+            const unsigned pos = atomicAdd(&myhist[hslot(bk[i])], 1u);
             staged[pos] = k[i];
-            stage_b[pos] = (unsigned short)c;
+            stage_b[pos] = (unsigned short)bk[i];
           }
         }
       }
