@@ -442,7 +442,10 @@ struct RadixReg {
   unsigned m;
   unsigned mul;
   __device__ __forceinline__ explicit RadixReg(const SplSmem<W>& S) : lo(S.lo), shift(S.shift), m((unsigned)S.m), mul(S.mul) {}
-  __device__ __forceinline__ int child(const W& x) const { return 2 * (int)radix_digit(x, lo, shift, mul, m); }
+  __device__ __forceinline__ int child(const W& x) const {
+    if constexpr (sizeof(W) == 8) return 2 * (int)radix_digit_hi(x, lo, shift, mul, m);  // (mode 3 only)
+    else return 2 * (int)radix_digit(x, lo, shift, mul, m);
+  }
 };
 
 template <typename W>
@@ -1168,7 +1171,9 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     int bk[ITEMS];
     unsigned wide = 0;
     const Xf<W> X = make_xf<W>(xf);
-    const bool radix = sizeof(W) <= 4 && S.use_tree == 2;  // recompute ids (cheap for <= 32-bit words)
+    // recompute child ids at write-out instead of staging them (cheap for
+    // <= 32-bit words and for the 64-bit high-word classifier)
+    const bool radix = (sizeof(W) <= 4 && S.use_tree == 2) || (sizeof(W) == 8 && S.use_tree == 3);
     auto classify_tile = [&](auto tree_tag, auto flt_tag) {
       constexpr int TREE = decltype(tree_tag)::value;
       constexpr bool FLT = decltype(flt_tag)::value;
