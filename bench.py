@@ -288,8 +288,10 @@ def roofline(prof, stats, n, kb, peak):
         a[0] += l
         a[1] += ms
     prof = {k: tuple(v) for k, v in agg.items()}
-    fin_l = sum(v[0] for k, v in prof.items() if k.startswith("k_final"))
-    fin_ms = sum(v[1] for k, v in prof.items() if k.startswith("k_final"))
+    fin_l = sum(v[0] for k, v in prof.items() if k.startswith("k_final") and k != "k_final_phase")
+    fin_ms = sum(v[1] for k, v in prof.items() if k.startswith("k_final") and k != "k_final_phase")
+    if "k_final_phase" in prof:  # wall time of the (partly concurrent) class launches
+        fin_ms = prof["k_final_phase"][1]
     per_kernel = {}
     for k in ("k_hist", "k_scatter"):
         if k in prof:
@@ -299,7 +301,7 @@ def roofline(prof, stats, n, kb, peak):
         # the base case is one phase launched per size class (most classes
         # are near-empty): count it as one launch per sort so the bytes of the
         # whole phase are divided by the whole phase's time
-        sorts = prof.get("k_init", (fin_l, 0.0))[0]
+        sorts = prof.get("k_final_phase", prof.get("k_init", (fin_l, 0.0)))[0]
         per_kernel["k_final"] = {"launches": sorts, "ms": fin_ms, "bytes_per_sort": bytes_["k_final"],
                                  "class_launches": fin_l}
     return per_kernel

@@ -49,11 +49,12 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // ---- optional per-kernel event timing (measurement tools only) -----------
 enum KernelId : int {
   K_INIT = 0, K_SAMPLE, K_HIST, K_SEGSCAN, K_PLAN, K_SCATTER, K_FINAL0, K_FINAL1, K_FINAL2, K_FINAL3, K_FINAL4,
-  K_FALLBACK, K_COPY, K_PART, K_MISC, K_COUNT
+  K_FALLBACK, K_COPY, K_PART, K_MISC, K_FINAL_PHASE, K_COUNT
 };
 const char* kKernelNames[K_COUNT] = {"k_init", "k_sample", "k_hist", "k_segscan", "k_plan", "k_scatter", "k_final_c0",
                                      "k_final_c1", "k_final_c2", "k_final_c3", "k_final_c4",
-                                     "k_final_fallback", "k_copy", "k_part", "k_misc"};
+                                     "k_final_fallback", "k_copy", "k_part", "k_misc",
+                                     "k_final_phase" /* wall time of all base-case launches of one sort */};
 struct Prof {
   bool on = false;
   std::mutex mu;
@@ -424,6 +425,7 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
     if (rs != VXS_OK) return rs;
     ++launches;
   }
+  ProfScope phase(K_FINAL_PHASE, st);  // (closes at the end of run_sort's final block)
   // The size classes and the equality-bucket copy touch disjoint items: the
   // class holding the most keys runs on the caller's stream, the rest on a
   // side stream underneath it (forked and joined with events, no host sync);
