@@ -10,16 +10,17 @@
 //                        random 4-key chunks per bucket, sorted in smem, m
 //                        equidistant splitters (m = 2^L - 1, L <= 8).
 //   partition.hpp:197-236 Partitioner::partition (2-way, <=pivot left)
-//                        -> k_hist + k_scatter: multiway classify with a
-//                        table-guided splitter search in smem, per-warp
-//                        shared-atomic ranking, block scan, smem-staged
+//                        -> k_hist + k_scatter: multiway classify (radix
+//                        digit, table-guided splitter search or tree in
+//                        smem), shared-atomic counts, block scan, smem-staged
 //                        buckets, coalesced bucket writes; each key is read
 //                        twice and written once per level.
 //   driver.hpp:142-151   degenerate recovery via scan_min_max -> equality
 //                        buckets: keys equal to a splitter land in a terminal
 //                        bucket, so all-equal / low-entropy inputs finish in
 //                        one level (no scan, no heapsort fallback).
-//   network.hpp:372-404  base case -> k_final (block_sort.cuh).
+//   network.hpp:372-404  base case -> k_final (block_sort.cuh bin_sort_item:
+//                        counting sort + odd-even transposition rounds).
 //
 // Every bucket owns a fixed index range [start, start+size) for its whole
 // life; keys ping-pong between the caller's array A and the temp array B in
@@ -1080,12 +1081,16 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
   }
 }
 
-// Scatter: classify again, rank each key within its (warp, child) with a
-// returning shared atomic on a per-warp histogram (one atomic per warp when
-// the warp's whole sub-tile falls into one child), scan across warps and
-// children, stage the tile in smem grouped by child (reusing the tile's TMA
-// stage), reserve each child's global range with one atomic per (tile,
-// child), then write each child run with consecutive threads (coalesced).
+// Scatter: classify again (radix digit / table / tree), count per child
+// with fire-and-forget shared atomics (one per warp when the warp's whole
+// sub-tile falls into one child), exclusive scan over the children, stage
+// the tile in smem grouped by child (each key takes the next slot of its
+// child with a returning atomic on the prefix; the tile's own TMA stage is
+// reused), advance this CTA's private per-child cursors (placement from the
+// k_hist / k_segscan offset table: no global atomics), then write each child
+// run with consecutive threads (coalesced), recomputing radix child ids
+// instead of staging them.  Exchange mode stores a segment's runs straight
+// into its owner's receive buffer (vxs_partition_exchange).
 template <typename W>
 __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) k_scatter(Params<W> P) {
   constexpr int THREADS = Cfg<W>::kScatThreads;
