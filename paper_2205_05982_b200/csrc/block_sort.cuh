@@ -14,9 +14,6 @@
 #pragma once
 #include "keys.cuh"
 
-#ifndef VXS_TWOPASS_U64  // build-time experiment switch (A/B timing); product: 0
-#define VXS_TWOPASS_U64 0
-#endif
 
 namespace vxs {
 
@@ -162,7 +159,8 @@ __device__ __forceinline__ void block_sort(W (&k)[ITEMS], W* smem) {
 // ---- counting-sort base case ------------------------------------------------
 // Keys of a final bucket are (close to) uniform over the bucket's range
 // [lo, hi]: the level above split by radix digit or by sample quantiles.  So
-// the base case is a counting sort on NB = 2*TOTAL linear bins of
+// the base case is a counting sort on NB linear bins (1x the capacity for
+// <= 4-byte keys, 2x for 8/16-byte keys: measured) of
 // (key - lo) >> shift, shift = bitlen(hi - lo) - log2 NB:
 //   1. block min/max, then one fire-and-forget shared atomic per key (bin
 //      counts);
@@ -187,9 +185,11 @@ __device__ __forceinline__ void block_sort(W (&k)[ITEMS], W* smem) {
 template <typename W, int THREADS, int ITEMS>
 struct BinSort {
   static constexpr int kTotal = THREADS * ITEMS;
-  static constexpr int kNB = kTotal <= 4096 ? 2 * kTotal : kTotal;
+  // bins per key slot: 1 for <= 4-byte keys (their odd-even rounds are one
+  // VIMNMX per key: fewer counters beat smaller bins), 2 for wider keys
+  static constexpr int kNB = (sizeof(W) <= 4 || kTotal > 4096) ? kTotal : 2 * kTotal;
   static constexpr int kBPT = kNB / THREADS;  // bins per thread in the scan
-  static constexpr int kNBBits = kNB == 512 ? 9 : kNB == 1024 ? 10 : kNB == 2048 ? 11 : kNB == 4096 ? 12 : kNB == 8192 ? 13 : 14;
+  static constexpr int kNBBits = kNB == 128 ? 7 : kNB == 256 ? 8 : kNB == 512 ? 9 : kNB == 1024 ? 10 : kNB == 2048 ? 11 : kNB == 4096 ? 12 : kNB == 8192 ? 13 : 14;
   // 8/16-byte keys: bin counters are 16-bit halves packed two per word (bin
   // b: word b/2, half b&1), half the smem of 32-bit counters for the zero
   // fill, the scan and its write-back (counts and prefixes are < 2^16).
@@ -199,7 +199,7 @@ struct BinSort {
   // ranks: 8-byte keys rank in the counting pass (one returning atomic per
   // key, measured best for them); the others count fire-and-forget and take
   // positions with a returning atomic on the prefixes in the scatter pass
-  static constexpr bool kTwoPass = sizeof(W) != 8 || VXS_TWOPASS_U64;
+  static constexpr bool kTwoPass = sizeof(W) != 8;
   static constexpr int kBinsPerWord = kPacked ? 2 : 1;
   static constexpr int kWords = kNB / kBinsPerWord;
   static constexpr int kWPT = kBPT / kBinsPerWord;  // words per thread in the scan
@@ -208,7 +208,7 @@ struct BinSort {
   static constexpr int kCnt = (kDummy + 4) & ~3;
   static constexpr int kMaxBin = 64;
   static constexpr size_t kSmem = (size_t)kTotal * sizeof(W) + (size_t)kCnt * 4;
-  static_assert((1 << kNBBits) == kNB && kWPT % 4 == 0 && kBPT <= 32, "bin count");
+  static_assert(kTotal < 1024 || ((1 << kNBBits) == kNB && kWPT % 4 == 0 && kBPT <= 32), "bin count");  // (class 0 never bins)
   // 4 pad words after every 32 counter words: the 16-byte groups of 8
   // threads in one LDS.128 phase land on distinct banks
   __host__ __device__ static __forceinline__ int wslot(int w) { return w + ((w >> 3) & ~3); }
