@@ -1217,23 +1217,24 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       for (int i = 0; i < ITEMS; ++i)
         if (bk[i] == -1) bk[i] = classify_slow(k[i], S);
     }
-    // count per child (fire-and-forget shared atomics; positions are taken in
-    // the staging pass with returning atomics on the prefixes); a warp whose
-    // whole sub-tile is one child counts (and later reserves) with one atomic
+    // rank within (warp, child); bk[] becomes child << 16 | rank
     bool same = bk[0] >= 0;
 #pragma unroll
     for (int i = 1; i < ITEMS; ++i) same = same && bk[i] == bk[0];
     const int b0 = __shfl_sync(0xffffffffu, bk[0], 0);
-    const bool uni = __all_sync(0xffffffffu, same && bk[0] == b0);
-    if (uni) {
-      if (lane == 0) atomicAdd(&myhist[hslot(b0)], 32u * ITEMS);
+    if (__all_sync(0xffffffffu, same && bk[0] == b0)) {
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(&myhist[hslot(b0)], 32u * ITEMS);
+      base = __shfl_sync(0xffffffffu, base, 0) + lane * ITEMS;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) bk[i] = (b0 << 16) | (int)(base + i);
     } else if (cnt == TILE) {  // full tile: every id is valid (straight-line code)
 #pragma unroll
-      for (int i = 0; i < ITEMS; ++i) atomicAdd(&myhist[hslot(bk[i])], 1u);
+      for (int i = 0; i < ITEMS; ++i) bk[i] = (bk[i] << 16) | (int)atomicAdd(&myhist[hslot(bk[i])], 1u);
     } else {
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i)
-        if (bk[i] >= 0) atomicAdd(&myhist[hslot(bk[i])], 1u);
+        if (bk[i] >= 0) bk[i] = (bk[i] << 16) | (int)atomicAdd(&myhist[hslot(bk[i])], 1u);
     }
     __syncthreads();
     // per child: exclusive prefix across warps, then across children; fold
@@ -1276,39 +1277,30 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       }
       __syncthreads();
       W* staged = reinterpret_cast<W*>(stage);
-      // stage grouped by child: each key takes the next slot of its child
-      // (returning shared atomic on the child's prefix)
-      if (uni) {
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(&myhist[hslot(b0)], 32u * ITEMS);
-        base = __shfl_sync(0xffffffffu, base, 0) + lane * ITEMS;
+      if (radix && cnt == TILE) {  // child ids are recomputed from the keys at write-out
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-          staged[base + i] = k[i];
-          if (!radix) stage_b[base + i] = (unsigned short)b0;
-        }
-      } else if (radix && cnt == TILE) {  // child ids are recomputed from the keys at write-out
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) staged[atomicAdd(&myhist[hslot(bk[i])], 1u)] = k[i];
+        for (int i = 0; i < ITEMS; ++i) staged[myhist[hslot(bk[i] >> 16)] + (unsigned)(bk[i] & 0xFFFF)] = k[i];
       } else if (radix) {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-          if (bk[i] >= 0) staged[atomicAdd(&myhist[hslot(bk[i])], 1u)] = k[i];
+          if (bk[i] >= 0) staged[myhist[hslot(bk[i] >> 16)] + (unsigned)(bk[i] & 0xFFFF)] = k[i];
         }
       } else if (cnt == TILE) {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-          const unsigned pos = atomicAdd(&myhist[hslot(bk[i])], 1u);
+          const int c = bk[i] >> 16;
+          const unsigned pos = myhist[hslot(c)] + (unsigned)(bk[i] & 0xFFFF);
           staged[pos] = k[i];
-          stage_b[pos] = (unsigned short)bk[i];
+          stage_b[pos] = (unsigned short)c;
         }
       } else {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
           if (bk[i] >= 0) {
-            const unsigned pos = atomicAdd(&myhist[hslot(bk[i])], 1u);
+            const int c = bk[i] >> 16;
+            const unsigned pos = myhist[hslot(c)] + (unsigned)(bk[i] & 0xFFFF);
             staged[pos] = k[i];
-            stage_b[pos] = (unsigned short)bk[i];
+            stage_b[pos] = (unsigned short)c;
           }
         }
       }
@@ -1416,8 +1408,13 @@ __global__ void __launch_bounds__(SortClass<CLS>::T, final_min_blocks<W, CLS>())
     if constexpr (CLS >= 1) {
       // counting-sort base case; items it rejects (clustered keys, decided
       // block-uniformly) go to the full-width network fallback kernel
-      const bool done = X.flt ? bin_sort_item<W, THREADS, ITEMS, true>(k, size, smem_raw, dst, X)
-                              : bin_sort_item<W, THREADS, ITEMS, false>(k, size, smem_raw, dst, X);
+      bool done;
+      if constexpr (sizeof(W) == 8)
+        done = X.flt ? bin_sort_item_rank<W, THREADS, ITEMS, true>(k, size, smem_raw, dst, X)
+                     : bin_sort_item_rank<W, THREADS, ITEMS, false>(k, size, smem_raw, dst, X);
+      else
+        done = X.flt ? bin_sort_item<W, THREADS, ITEMS, true>(k, size, smem_raw, dst, X)
+                     : bin_sort_item<W, THREADS, ITEMS, false>(k, size, smem_raw, dst, X);
       if (!done && threadIdx.x == 0) {
         const unsigned long long slot = atomicAdd(&P.ctrl->item_count[kListFallback], 1ull);
         if (slot < P.cap_items) P.items[kListFallback][slot] = item;
