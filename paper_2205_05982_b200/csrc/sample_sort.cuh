@@ -1228,6 +1228,21 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       base = __shfl_sync(0xffffffffu, base, 0) + lane * ITEMS;
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) bk[i] = (b0 << 16) | (int)(base + i);
+    } else if (cnt == TILE && __shfl_sync(0xffffffffu, bk[0], 31) == b0) {
+      // presorted-looking warp (its first 32-key slice is one child): rank
+      // slice by slice, one atomic per uniform slice -- 32 lanes would
+      // otherwise serialise on the same counter
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int ci = __shfl_sync(0xffffffffu, bk[i], 0);
+        if (__all_sync(0xffffffffu, bk[i] == ci)) {
+          unsigned base = 0;
+          if (lane == 0) base = atomicAdd(&myhist[hslot(ci)], 32u);
+          bk[i] = (ci << 16) | (int)(__shfl_sync(0xffffffffu, base, 0) + lane);
+        } else {
+          bk[i] = (bk[i] << 16) | (int)atomicAdd(&myhist[hslot(bk[i])], 1u);
+        }
+      }
     } else if (cnt == TILE) {  // full tile: every id is valid (straight-line code)
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) bk[i] = (bk[i] << 16) | (int)atomicAdd(&myhist[hslot(bk[i])], 1u);
