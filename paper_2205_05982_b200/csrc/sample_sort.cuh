@@ -674,24 +674,43 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
   }
 }
 
-// Tile t of the current level: owning bucket (advanced from p), first key and
-// key count.  All threads compute the same values.
+// Tile t of the current level: owning bucket, first key and key count.
 struct TileRef {
   int p;
   unsigned long long lo;
   int cnt;
 };
+
+// The issuing thread's walk over tiles: the owning bucket's descriptor and
+// the next bucket's first tile stay in registers, so issuing tile t+1 costs
+// no dependent global loads except at bucket boundaries.
 template <typename W>
-__device__ __forceinline__ TileRef tile_ref(const SplitDesc* list, int nb, int p, unsigned long long t) {
-  while (p + 1 < nb && list[p + 1].tile_base <= t) ++p;
-  const SplitDesc& d = list[p];
-  TileRef r;
-  r.p = p;
-  r.lo = d.start + (t - d.tile_base) * (unsigned long long)Cfg<W>::kTile;
-  const unsigned long long end = d.start + d.size;
-  r.cnt = (int)((end - r.lo) < (unsigned long long)Cfg<W>::kTile ? (end - r.lo) : Cfg<W>::kTile);
-  return r;
-}
+struct TileCursor {
+  int p;
+  unsigned flags;
+  unsigned long long start, size, tb, next_tb;
+  __device__ __forceinline__ void load(const SplitDesc* list, int nb) {
+    const SplitDesc d = list[p];
+    start = d.start;
+    size = d.size;
+    tb = d.tile_base;
+    flags = d.flags;
+    next_tb = p + 1 < nb ? list[p + 1].tile_base : ~0ull;
+  }
+  __device__ __forceinline__ TileRef at(const SplitDesc* list, int nb, unsigned long long t) {
+    if (t >= next_tb) {
+      ++p;
+      while (p + 1 < nb && list[p + 1].tile_base <= t) ++p;
+      load(list, nb);
+    }
+    TileRef r;
+    r.p = p;
+    r.lo = start + (t - tb) * (unsigned long long)Cfg<W>::kTile;
+    const unsigned long long end = start + size;
+    r.cnt = (int)((end - r.lo) < (unsigned long long)Cfg<W>::kTile ? (end - r.lo) : Cfg<W>::kTile);
+    return r;
+  }
+};
 
 template <typename W>
 __device__ __forceinline__ const W* src_of(const Params<W>& P, unsigned flags) {
@@ -727,16 +746,16 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
   const unsigned long long t1 = t0 + tpc < T ? t0 + tpc : T;
   if (t0 >= t1) return;
   const SplitDesc* list = P.split[P.cur];
-  int p_issue = 0;
+  TileCursor<W> ic;  // (thread 0: the tile issuer)
   if (threadIdx.x == 0) {
     s_p = find_bucket(list, nb, t0);
     for (int s = 0; s < Cfg<W>::kHistStages; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    p_issue = s_p;
+    ic.p = s_p;
+    ic.load(list, nb);
     for (int s = 0; s + 1 < Cfg<W>::kHistStages && t0 + s < t1; ++s) {  // prefetch depth Cfg<W>::kHistStages - 1
-      const TileRef r = tile_ref<W>(list, nb, p_issue, t0 + s);
-      p_issue = r.p;
-      tile_issue(src_of(P, list[r.p].flags) + r.lo, (unsigned long long)r.cnt * sizeof(W),
+      const TileRef r = ic.at(list, nb, t0 + s);
+      tile_issue(src_of(P, ic.flags) + r.lo, (unsigned long long)r.cnt * sizeof(W),
                  smem_raw + s * stage_bytes<W>(), &bars[s]);
     }
   }
@@ -744,6 +763,7 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
   __syncthreads();
   int p = s_p;
   SplitDesc d = list[p];
+  unsigned long long p_next = p + 1 < nb ? list[p + 1].tile_base : ~0ull;  // next bucket's first tile
   int L = (int)(d.L & 0xFFu);
   load_splitters(P.splitters + (unsigned long long)p * 256, d.L, S, d.aux);
   unsigned phase = 0;
@@ -752,12 +772,11 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
     if (threadIdx.x == 0 && t + Cfg<W>::kHistStages - 1 < t1) {
       // the stage consumed in the previous iteration (freed by its final barrier)
       const int sn = st == 0 ? Cfg<W>::kHistStages - 1 : st - 1;
-      const TileRef r = tile_ref<W>(list, nb, p_issue, t + Cfg<W>::kHistStages - 1);
-      p_issue = r.p;
-      tile_issue(src_of(P, list[r.p].flags) + r.lo, (unsigned long long)r.cnt * sizeof(W),
+      const TileRef r = ic.at(list, nb, t + Cfg<W>::kHistStages - 1);
+      tile_issue(src_of(P, ic.flags) + r.lo, (unsigned long long)r.cnt * sizeof(W),
                  smem_raw + sn * stage_bytes<W>(), &bars[sn]);
     }
-    if (p + 1 < nb && list[p + 1].tile_base <= t) {
+    if (t >= p_next) {
       // flush and move to the next bucket
       const int nc = num_children(L);
       unsigned long long* sg = P.seg + (unsigned long long)(p + blockIdx.x) * kChildStride;
@@ -767,6 +786,7 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
       }
       while (p + 1 < nb && list[p + 1].tile_base <= t) ++p;
       d = list[p];
+      p_next = p + 1 < nb ? list[p + 1].tile_base : ~0ull;
       L = (int)(d.L & 0xFFu);
       __syncthreads();
       load_splitters(P.splitters + (unsigned long long)p * 256, d.L, S, d.aux);
@@ -1116,18 +1136,20 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   const unsigned long long t1 = t0 + tpc < T ? t0 + tpc : T;
   if (t0 >= t1) return;
   const SplitDesc* list = P.split[P.cur];
-  int p_issue = 0;
+  TileCursor<W> ic;  // (thread 0: the tile issuer)
   if (threadIdx.x == 0) {
     s_p = find_bucket(list, nb, t0);
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    p_issue = s_p;
-    const TileRef r = tile_ref<W>(list, nb, p_issue, t0);
-    tile_issue(src_of(P, list[r.p].flags) + r.lo, (unsigned long long)r.cnt * sizeof(W), smem_raw, &bars[0]);
+    ic.p = s_p;
+    ic.load(list, nb);
+    const TileRef r = ic.at(list, nb, t0);
+    tile_issue(src_of(P, ic.flags) + r.lo, (unsigned long long)r.cnt * sizeof(W), smem_raw, &bars[0]);
   }
   __syncthreads();
   int p = s_p;
   SplitDesc d = list[p];
+  unsigned long long p_next = p + 1 < nb ? list[p + 1].tile_base : ~0ull;  // next bucket's first tile
   int L = (int)(d.L & 0xFFu);
   load_splitters(P.splitters + (unsigned long long)p * 256, d.L, S, d.aux);
   auto load_cursors = [&]() {
@@ -1145,14 +1167,14 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   for (unsigned long long t = t0; t < t1; ++t) {
     const int st = (int)((t - t0) & (kStages - 1));
     if (threadIdx.x == 0 && t + 1 < t1) {
-      const TileRef r = tile_ref<W>(list, nb, p_issue, t + 1);
-      p_issue = r.p;
-      tile_issue(src_of(P, list[r.p].flags) + r.lo, (unsigned long long)r.cnt * sizeof(W),
+      const TileRef r = ic.at(list, nb, t + 1);
+      tile_issue(src_of(P, ic.flags) + r.lo, (unsigned long long)r.cnt * sizeof(W),
                  smem_raw + (st ^ 1) * stage_bytes<W>(), &bars[st ^ 1]);
     }
-    if (p + 1 < nb && list[p + 1].tile_base <= t) {
+    if (t >= p_next) {
       while (p + 1 < nb && list[p + 1].tile_base <= t) ++p;
       d = list[p];
+      p_next = p + 1 < nb ? list[p + 1].tile_base : ~0ull;
       L = (int)(d.L & 0xFFu);
       load_splitters(P.splitters + (unsigned long long)p * 256, d.L, S, d.aux);
       load_cursors();
