@@ -1419,8 +1419,13 @@ __global__ void __launch_bounds__(SortClass<CLS>::T, final_min_blocks<W, CLS>())
   const unsigned long long nitems = P.ctrl->item_count[CLS];
   const Item* items = P.items[CLS];
   const Xf<W> X = make_xf<W>(P.xf);
+  // the next item's descriptor is loaded while this one is sorted (one
+  // dependent global round trip fewer per item)
+  Item nxt{};
+  if (blockIdx.x < nitems) nxt = items[blockIdx.x];
   for (unsigned long long it = blockIdx.x; it < nitems; it += gridDim.x) {
-    const Item item = items[it];
+    const Item item = nxt;
+    if (it + gridDim.x < nitems) nxt = items[it + gridDim.x];
     const W* src = (item.flags & F_IN_B) ? P.b : P.a;
     const int size = (int)item.size;
     W k[ITEMS];
@@ -1484,8 +1489,13 @@ __global__ void __launch_bounds__(SortClass<4>::T) k_final_fallback(Params<W> P)
   const unsigned long long nitems = P.ctrl->item_count[kListFallback];
   const Item* items = P.items[kListFallback];
   const Xf<W> X = make_xf<W>(P.xf);
+  // the next item's descriptor is loaded while this one is sorted (one
+  // dependent global round trip fewer per item)
+  Item nxt{};
+  if (blockIdx.x < nitems) nxt = items[blockIdx.x];
   for (unsigned long long it = blockIdx.x; it < nitems; it += gridDim.x) {
-    const Item item = items[it];
+    const Item item = nxt;
+    if (it + gridDim.x < nitems) nxt = items[it + gridDim.x];
     const W* src = (item.flags & F_IN_B) ? P.b : P.a;
     const int size = (int)item.size;
     W k[ITEMS];
