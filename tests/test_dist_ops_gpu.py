@@ -126,3 +126,47 @@ def test_fused_exchange_virtual_ranks(cuda, kt, desc, world):
     assert got.tobytes() == want.tobytes()
     if kt in ("u64", "u32", "i32", "i64"):
         assert max(recv) < 1.5 * sum(recv) / world  # sampled splitters balance the ranks
+
+
+def _ipc_child(handle, nbytes, q):
+    import torch
+    import paper_2205_05982_b200 as vx2
+    torch.cuda.set_device(0)
+    try:
+        blk = vx2.DeviceBlock.open(handle, nbytes)
+        t = blk.tensor()
+        q.put(int(t[:4096].view(torch.int32).sum().item()))
+        t[:4096].view(torch.int32).fill_(7)  # write through the mapping
+        torch.cuda.synchronize()
+        blk.close()
+        q.put("ok")
+    except Exception as e:  # noqa: BLE001
+        q.put(repr(e))
+
+
+def test_device_block_ipc(cuda):
+    """The fused exchange's symmetric window plumbing: an IPC-exported block
+    (vxs_device_alloc / vxs_ipc_handle), viewed as a tensor through
+    __cuda_array_interface__, mapped by another process (vxs_ipc_open) that
+    reads and writes it -- no kernel waits on another process."""
+    import torch.multiprocessing as mp
+    nbytes = 1 << 20
+    blk = vx.DeviceBlock(nbytes)
+    t = blk.tensor()
+    assert t.numel() == nbytes and t.device.type == "cuda" and t.data_ptr() == blk.ptr
+    t.view(torch.int32)[:1024].fill_(3)
+    t.view(torch.int32)[1024:].zero_()
+    torch.cuda.synchronize()
+    h = blk.handle()
+    assert isinstance(h, bytes) and len(h) == 64
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_ipc_child, args=(h, nbytes, q))
+    p.start()
+    got = q.get(timeout=120)
+    status = q.get(timeout=120)
+    p.join(timeout=60)
+    assert status == "ok", status
+    assert got == 3 * 1024
+    assert int(t[:4096].view(torch.int32).sum().item()) == 7 * 1024
+    blk.close()
