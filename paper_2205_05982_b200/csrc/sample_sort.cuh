@@ -195,6 +195,16 @@ struct Params {
   const unsigned long long* xoff;
 };
 
+// Programmatic dependent launch: the host may launch the next kernel of the
+// chain early (PDL attribute); every kernel first waits for its predecessor
+// to complete (griddepcontrol.wait -- a no-op without PDL) and then lets its
+// own successor be scheduled.  All grids here are a single resident wave,
+// so early-scheduled successors only take SM slots the tail frees.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   z += 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -524,6 +534,7 @@ __global__ void k_init(Params<W> P) {
 // PAPER.md:393-398), smem bitonic sort, equidistant splitters.
 template <typename W, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
+  pdl_enter();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   W* s = reinterpret_cast<W*>(smem_raw);
   __shared__ unsigned dcnt[1 << kMaxRadixL];
@@ -729,6 +740,7 @@ __host__ __device__ constexpr int stage_bytes() {
 // child (low-entropy input) adds 32 with a single atomic.
 template <typename W>
 __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) k_hist(Params<W> P) {
+  pdl_enter();
   constexpr int THREADS = Cfg<W>::kHistThreads;
   constexpr int TILE = Cfg<W>::kTile;
   constexpr int ITEMS = TILE / THREADS;
@@ -874,6 +886,7 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
 // one warp per item, 16 independent loads in flight per lane.
 template <typename W>
 __global__ void __launch_bounds__(128) k_segscan(Params<W> P) {
+  pdl_enter();
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
   const int nb = (int)(packed >> 40);
   const unsigned long long T = packed & kTileMask;
@@ -916,6 +929,7 @@ __global__ void __launch_bounds__(128) k_segscan(Params<W> P) {
 // round trip of loads instead of a serial walk down ~300 rows per lane).
 template <typename W>
 __global__ void __launch_bounds__(1024) k_segscan_root(Params<W> P) {
+  pdl_enter();
   __shared__ unsigned long long part[32][33];
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
   if ((int)(packed >> 40) == 0) return;
@@ -965,6 +979,7 @@ __global__ void __launch_bounds__(1024) k_segscan_root(Params<W> P) {
 // item of <= Cap keys) or copy items (equality buckets).
 template <typename W>
 __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
+  pdl_enter();
   constexpr int THREADS = kChildStride;
   constexpr unsigned long long CAP = Cfg<W>::kCap;
   __shared__ unsigned long long s_cnt[kChildStride];
@@ -1113,6 +1128,7 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
 // into its owner's receive buffer (vxs_partition_exchange).
 template <typename W>
 __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) k_scatter(Params<W> P) {
+  pdl_enter();
   constexpr int THREADS = Cfg<W>::kScatThreads;
   constexpr int TILE = Cfg<W>::kTile;
   constexpr int ITEMS = TILE / THREADS;
@@ -1412,6 +1428,7 @@ constexpr int final_min_blocks() {
 // write back into A.
 template <typename W, int CLS>
 __global__ void __launch_bounds__(SortClass<CLS>::T, final_min_blocks<W, CLS>()) k_final(Params<W> P) {
+  pdl_enter();
   constexpr int THREADS = SortClass<CLS>::T;
   constexpr int ITEMS = SortClass<CLS>::I;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1482,6 +1499,7 @@ __global__ void __launch_bounds__(SortClass<CLS>::T, final_min_blocks<W, CLS>())
 // (persistent; reads the fallback count on the device, usually zero).
 template <typename W>
 __global__ void __launch_bounds__(SortClass<4>::T) k_final_fallback(Params<W> P) {
+  pdl_enter();
   constexpr int THREADS = SortClass<4>::T;
   constexpr int ITEMS = (sizeof(W) >= 16) ? 8 : 16;  // capacity >= Cap
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1520,6 +1538,7 @@ __global__ void __launch_bounds__(SortClass<4>::T) k_final_fallback(Params<W> P)
 // of single keys, B -> A or decode-in-place in A.
 template <typename W>
 __global__ void __launch_bounds__(256) k_copy(Params<W> P) {
+  pdl_enter();
   // small items: one CTA per item
   {
     const unsigned long long nitems = P.ctrl->item_count[kListCopySmall];

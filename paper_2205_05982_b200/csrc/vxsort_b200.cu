@@ -238,6 +238,28 @@ int expected_levels(size_t n, size_t cap) {
   return lv;
 }
 
+// Launch with programmatic stream serialization (the kernels open with
+// pdl_enter); plain launch while per-kernel profiling events sit between
+// launches.
+template <typename PT>
+void pdl_launch(void (*fn)(PT), int grid, int block, size_t smem, cudaStream_t st, const PT& P) {
+  if (g_prof.on) {
+    fn<<<grid, block, smem, st>>>(P);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, fn, P);
+}
+
 template <typename W>
 vxs_status launch_level(Params<W>& P, cudaStream_t st, int& launches) {
   constexpr int kSampleThreads = 512;
@@ -245,33 +267,33 @@ vxs_status launch_level(Params<W>& P, cudaStream_t st, int& launches) {
     ProfScope ps(K_SAMPLE + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
     auto fn = k_sample<W, kSampleThreads>;
     const int g = grid_for((const void*)fn, kSampleThreads, sample_smem<W>());
-    fn<<<g, kSampleThreads, sample_smem<W>(), st>>>(P);
+    pdl_launch(fn, g, kSampleThreads, sample_smem<W>(), st, P);
   }
   {
     ProfScope ps(K_HIST + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
     auto fn = k_hist<W>;
-    fn<<<P.grid, Cfg<W>::kHistThreads, hist_smem<W>(), st>>>(P);
+    pdl_launch(fn, P.grid, Cfg<W>::kHistThreads, hist_smem<W>(), st, P);
   }
   {
     ProfScope ps(K_SEGSCAN + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
     if (P.level == 0) {  // the root bucket: every CTA holds a row
-      k_segscan_root<W><<<(kChildStride + 31) / 32, 1024, 0, st>>>(P);
+      pdl_launch(k_segscan_root<W>, (kChildStride + 31) / 32, 1024, 0, st, P);
     } else {
       auto fn = k_segscan<W>;
       const int g = grid_for((const void*)fn, 128, 0);
-      fn<<<g, 128, 0, st>>>(P);
+      pdl_launch(fn, g, 128, 0, st, P);
     }
   }
   {
     ProfScope ps(K_PLAN + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
     auto fn = k_plan<W>;
     const int g = grid_for((const void*)fn, kChildStride, 0);
-    fn<<<g, kChildStride, 0, st>>>(P);
+    pdl_launch(fn, g, kChildStride, 0, st, P);
   }
   {
     ProfScope ps(K_SCATTER + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
     auto fn = k_scatter<W>;
-    fn<<<P.grid, Cfg<W>::kScatThreads, scatter_smem<W>(), st>>>(P);
+    pdl_launch(fn, P.grid, Cfg<W>::kScatThreads, scatter_smem<W>(), st, P);
   }
   launches += 5;
   VXS_CK(cudaGetLastError(), "level launch");
