@@ -760,9 +760,11 @@ void chunk_bounds(size_t n, int C, ChunkSet& cs) {
   cs.C = C;
   double w[kPipeMaxChunks];
   double tot = 0;
+  int taper = 3;  // the last chunks shrink (1/2, 1/4, 1/8): the sort exposed after the last H2D is short
+  if (const char* e = std::getenv("VXSORT_HOST_TAPER")) taper = std::atoi(e);
   for (int c = 0; c < C; ++c) {
     const int from_end = C - 1 - c;
-    w[c] = (C >= 6 && from_end < 3) ? 1.0 / (double)(1 << (3 - from_end)) : 1.0;  // 1/2, 1/4, 1/8
+    w[c] = (C >= 6 && from_end < taper) ? 1.0 / (double)(1 << (taper - from_end)) : 1.0;
     tot += w[c];
   }
   double acc = 0;
