@@ -62,8 +62,8 @@ class SymmetricWindow:
             return
         nbytes = max(nbytes, int(self.nbytes * 1.25))
         nbytes = (nbytes + (1 << 21) - 1) & ~((1 << 21) - 1)
-        self.close()
         torch.cuda.synchronize(device)
+        self.close(group)
         self.mine = DeviceBlock(nbytes)
         handles = [None] * dist.get_world_size(group)
         dist.all_gather_object(handles, self.mine.handle(), group=group)
@@ -75,11 +75,15 @@ class SymmetricWindow:
     def local(self):
         return self.mine.tensor()
 
-    def close(self):
+    def close(self, group=None):
+        # every rank unmaps its peers' blocks before any owner frees its own
+        # (freeing an exported block that is still mapped elsewhere is undefined)
         for b in self.peers:
             if b is not self.mine:
                 b.close()
         if self.mine is not None:
+            if dist.is_initialized():
+                dist.barrier(group=group)
             self.mine.close()
         self.peers, self.mine, self.nbytes = [], None, 0
 
