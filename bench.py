@@ -36,7 +36,10 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-KEYS_PER_CPU_INSTANCE = 10_000_000
+DEFAULT_SINGLE = "c2-u32-asc"   # BASELINE configs[1], first case (the metric's headline)
+DEFAULT_DIST = "c5"              # BASELINE configs[4]: u64, 2^30 keys per GPU
+DEFAULT_EXTRAS = ("u64-uniform,c2-u32-desc,c2-f32-asc,c2-f32-desc,c1,c3a,c3b,c3c,c3d,c3e,c3f,c4a,c4b,"
+                  "c5,c5-skew,partition-u32,partition-u64")
 
 
 def log(*a):
@@ -127,24 +130,52 @@ def to_device(x, kt):
 
 
 def check_sorted_device(buf, kt, desc, src=None):
-    """Device-side validation of a sorted result: non-decreasing in the
-    order-transformed domain, and the same multiset fingerprint as the input."""
+    """Device-side validation of a sorted result, independent of the
+    product's key transform: integers by their own (signed / unsigned) order,
+    128-bit keys by (hi, lo) unsigned, floats by IEEE value with NaNs last in
+    both orders and -0.0 before +0.0 ascending (after it descending) -- the
+    canonical order of SURVEY §8c; plus the same multiset fingerprint as the
+    input."""
     import torch
-    import paper_2205_05982_b200 as vx
-    w = buf.clone()
-    vx.transform(w, vx.Order(int(desc)), key_type=kt if kt in ("k128", "kv64") else None)
-    kb = vx.KEY_BYTES[kt]
-    if kb == 16:
-        hi = w[:, 1].view(torch.int64) ^ torch.iinfo(torch.int64).min
-        lo = w[:, 0].view(torch.int64) ^ torch.iinfo(torch.int64).min
-        ok = bool(((hi[1:] > hi[:-1]) | ((hi[1:] == hi[:-1]) & (lo[1:] >= lo[:-1]))).all())
-    else:
-        sdt = {2: torch.int16, 4: torch.int32, 8: torch.int64}[kb]
-        s = w.view(sdt) ^ torch.iinfo(sdt).min
-        ok = bool((s[1:] >= s[:-1]).all())
+    kb = KEY_BYTES[kt]
+    n = buf.shape[0]
+    ok = True
+    if n > 1:
+        if kb == 16:
+            hi = buf[:, 1].view(torch.int64) ^ torch.iinfo(torch.int64).min
+            lo = buf[:, 0].view(torch.int64) ^ torch.iinfo(torch.int64).min
+            if desc:
+                ok = bool(((hi[1:] < hi[:-1]) | ((hi[1:] == hi[:-1]) & (lo[1:] <= lo[:-1]))).all())
+            else:
+                ok = bool(((hi[1:] > hi[:-1]) | ((hi[1:] == hi[:-1]) & (lo[1:] >= lo[:-1]))).all())
+            if kt == "kv64":  # stable: payload (lo) ascends inside equal keys in both orders
+                tie = hi[1:] == hi[:-1]
+                ok = ok and bool((lo[1:][tie] > lo[:-1][tie]).all())
+        elif kt in ("f32", "f64"):
+            nan = torch.isnan(buf)
+            nn = int(nan.sum())
+            v = buf[:n - nn]
+            ok = bool(nan[n - nn:].all())
+            ok = ok and bool(((v[1:] <= v[:-1]) if desc else (v[1:] >= v[:-1])).all())
+            z = v[v == 0]
+            if z.numel() > 1:
+                sgn = torch.signbit(z).to(torch.int8)
+                d = sgn[1:] - sgn[:-1]
+                ok = ok and bool(((d >= 0) if desc else (d <= 0)).all())
+        else:
+            if kt[0] == "u":  # unsigned: flip the sign bit to compare as signed
+                sdt = {2: torch.int16, 4: torch.int32, 8: torch.int64}[kb]
+                s = buf.view(sdt) ^ torch.iinfo(sdt).min
+            else:
+                s = buf
+            ok = bool(((s[1:] <= s[:-1]) if desc else (s[1:] >= s[:-1])).all())
     if src is not None:
         ok = ok and fingerprint(buf, kb) == fingerprint(src, kb)
     return ok
+
+
+KEY_BYTES = {"i16": 2, "u16": 2, "i32": 4, "u32": 4, "f32": 4, "i64": 8, "u64": 8, "f64": 8,
+             "k128": 16, "kv64": 16}
 
 
 def fingerprint(t, kb):
@@ -175,50 +206,78 @@ def algorithmic_bytes(stats, n, kb):
 
 
 # ---------------------------------------------------------------- CPU leg ----
-def cpu_reference_run(x, kt, desc, instances, n_each, reps):
-    """Independent-instance throughput of the reference's own vexsort::sort
-    (harness.cpp:316-358 threads mode) over `instances` host threads."""
+def _ref_input(x, kt):
+    okt = "k128" if kt == "kv64" else kt
+    if okt in ("f32", "f64") and np.isnan(x).any():
+        x = x.copy()
+        x[np.isnan(x)] = np.inf  # the reference rejects NaN (driver.hpp:176-180)
+    return x, okt
+
+
+def _host_budget_bytes():
+    try:
+        import psutil
+        return int(psutil.virtual_memory().available * 0.5)
+    except Exception:  # noqa: BLE001
+        return 16 << 30
+
+
+def cpu_instances(x, kt, desc, instances, reps):
+    """The reference's harness threads mode (harness.cpp:316-358): `instances`
+    threads, each sorting its own FULL-SIZE copy of the input with
+    vexsort::sort; aggregate throughput = instances * n / wall time of the
+    slowest.  Returns (per-rep wall times, kind)."""
     import ctypes
     import oracle
     use_ref = oracle.ref_available()
-    okt = "k128" if kt == "kv64" else kt
-    n_total = x.shape[0]
-    bufs = []
-    for i in range(instances):
-        s = (i * n_each) % max(1, n_total - n_each + 1)
-        bufs.append(np.ascontiguousarray(x[s:s + n_each]).copy())
-    pristine = [b.copy() for b in bufs]
-    if okt in ("f32", "f64"):
-        for b in bufs + pristine:  # the reference rejects NaN (driver.hpp:176-180)
-            b[np.isnan(b)] = np.inf
+    x, okt = _ref_input(x, kt)
+    n = x.shape[0]
+    bufs = [np.empty_like(x) for _ in range(instances)]
     times = []
-    for r in range(reps):
-        for b, p in zip(bufs, pristine):
-            b[...] = p
+    for _ in range(reps):
+        for b in bufs:
+            b[...] = x
         ptrs = (ctypes.c_void_p * instances)(*[b.ctypes.data for b in bufs])
         t0 = time.perf_counter()
         if use_ref:
-            rc = oracle.ref().ref_sort_instances(ptrs, instances, n_each, oracle.KEY_CODE[okt], int(desc), 1)
+            rc = oracle.ref().ref_sort_instances(ptrs, instances, n, oracle.KEY_CODE[okt], int(desc), 1)
             assert rc == 0, oracle.ref().ref_last_error()
         else:
             from concurrent.futures import ThreadPoolExecutor
             with ThreadPoolExecutor(instances) as ex:
-                list(ex.map(lambda b: oracle.lib().vxo_sort(b.ctypes.data, n_each, oracle.KEY_CODE[okt],
+                list(ex.map(lambda b: oracle.lib().vxo_sort(b.ctypes.data, n, oracle.KEY_CODE[okt],
                                                              int(desc), 1, None), bufs))
         times.append(time.perf_counter() - t0)
     return times, ("reference" if use_ref else "port")
 
 
-def cpu_baseline(x, kt, desc):
-    cores = os.cpu_count() or 1
-    n_each = min(KEYS_PER_CPU_INSTANCE, x.shape[0])
-    times, kind = cpu_reference_run(x, kt, desc, cores, n_each, reps=2)
-    t = statistics.median(times)
-    one, _ = cpu_reference_run(x, kt, desc, 1, n_each, reps=1)
-    return {"value": round(cores * n_each / t / 1e6, 2), "unit": "Mkeys/s", "cores": cores, "kind": kind,
-            "sample": f"{cores} independent instances x {n_each} keys of the same workload "
-                      f"(vexsort::sort, harness threads mode); median of 2 reps",
-            "single_core_mkeys_s": round(n_each / one[0] / 1e6, 2)}
+def cpu_isa():
+    import oracle
+    if not oracle.ref_available():
+        return "oracle port (scalar C)"
+    return oracle.ref().ref_isa().decode()
+
+
+def max_instances(x):
+    return max(1, min(os.cpu_count() or 1, _host_budget_bytes() // max(1, x.nbytes)))
+
+
+def cpu_baseline(x, kt, desc, single_reps=10, agg_reps=2):
+    """Same config as the GPU line: the reference on the FULL input (1 core,
+    median of `single_reps`, harness.cpp:300-315) and the harness's
+    independent-instances aggregate over all host cores (full-size copies)."""
+    n = x.shape[0]
+    one, kind = cpu_instances(x, kt, desc, 1, single_reps)
+    cores = max_instances(x)
+    agg, _ = cpu_instances(x, kt, desc, cores, agg_reps)
+    t = statistics.median(agg)
+    return {"value": round(cores * n / t / 1e6, 2), "unit": "Mkeys/s", "cores": cores, "kind": kind,
+            "sample": f"{cores} independent vexsort::sort instances, each on a full-size copy of the workload "
+                      f"({n} keys; harness threads mode, harness.cpp:316-358), median of {agg_reps} reps; "
+                      f"NaN -> +inf for the reference (it rejects NaN)",
+            "single_core_mkeys_s": round(n / statistics.median(one) / 1e6, 2),
+            "single_core_sample": f"1 core, full {n} keys, median of {single_reps} reps (harness.cpp:300-315)",
+            "isa": cpu_isa()}
 
 
 # ---------------------------------------------------------------- GPU leg ----
@@ -317,15 +376,126 @@ def ncu_traffic():
     return None
 
 
+DEVICE_GEN = ("c5", "c5-skew")  # 8 GB inputs: generated on the device (same SplitMix64 bits)
+
+
+def load_workload(name, n=None, rank=0):
+    """(device keys, host keys or None, key type, descending)."""
+    import torch
+    from paper_2205_05982_b200 import workloads
+    if name in DEVICE_GEN:
+        d, kt, desc = workloads.make_device(name, n=n, rank=rank, device="cuda")
+        return d, None, kt, desc
+    x, kt, desc = workloads.make(name, n=n, rank=rank)
+    return torch.from_numpy(x).to("cuda"), x, kt, desc
+
+
+def time_extra(wl, peak, steps=3):
+    """One extra workload: validated, timed (device-resident), per-kernel split."""
+    import torch
+    import paper_2205_05982_b200 as vx
+    se, _, kte, de = load_workload(wl)
+    ne = se.shape[0]
+    be = torch.empty_like(se)
+    wse = torch.empty(vx.workspace_bytes(ne, kte), dtype=torch.uint8, device="cuda")
+    be.copy_(se)
+    vx.sort(be, vx.SortConfig(order=vx.Order(int(de)), seed=1),
+            key_type=kte if kte in ("k128", "kv64") else None, workspace=wse)
+    torch.cuda.synchronize()
+    okx = check_sorted_device(be, kte, de, se)
+    te, _, ste, _ = gpu_time_sorts(be, se, wse, kte, de, steps, 2)
+    _, _, _, pre = gpu_time_sorts(be, se, wse, kte, de, steps, 1, profile=True)
+    mse = statistics.mean(te)
+    kbe = KEY_BYTES[kte]
+    pe = roofline(pre, ste, ne, kbe, peak)
+    sc = pe.get("k_scatter")
+    out = {"mkeys_s": round(ne / (mse * 1e-3) / 1e6, 2), "ms": round(mse, 3), "n": ne, "key_type": kte,
+           "order": "desc" if de else "asc",
+           "gb_per_s_sorted": round(ne * kbe / (mse * 1e-3) / 1e9, 2), "validated": okx,
+           "levels": ste.max_depth, "fallback_triggered": bool(ste.fallback_triggered),
+           "design_hbm_frac": round(algorithmic_bytes(ste, ne, kbe)["total"] / (mse * 1e-3) / 1e9 / peak, 4),
+           "ideal_one_pass_frac": round(2 * ne * kbe / (mse * 1e-3) / 1e9 / peak, 4),
+           "scatter_frac": (round(sc["bytes_per_sort"] / (sc["ms"] / steps * 1e-3) / 1e9 / peak, 4)
+                            if sc else None),
+           "kernels_ms": {k: round(v[1] / steps, 4) for k, v in pre.items()}}
+    del se, be, wse
+    torch.cuda.empty_cache()
+    return out
+
+
+def time_partition(kt, peak, n=100_000_000, steps=5):
+    """Partition-only benchmark (the analogue of the reference's
+    run_partition_bench, harness.cpp:409-489): vxs_partition of n uniform keys
+    by 255 sample splitters (one classify + scatter level: hist read + scatter
+    read/write = 3*N*s bytes), validated, next to the reference's own 2-way
+    partition bench on the host."""
+    import torch
+    import paper_2205_05982_b200 as vx
+    name = "u64-uniform" if kt == "u64" else "c2-u32-asc"
+    src, _, _, _ = load_workload(name, n=n)
+    kb = KEY_BYTES[kt]
+    spl = vx.sample(src, 4096, seed=3)
+    vx.sort(spl, vx.SortConfig(seed=1))
+    spl = spl.view(torch.int64 if kb == 8 else torch.int32)[16::16][:255].contiguous().view(src.dtype)
+    out = torch.empty_like(src)
+    _, counts = vx.partition(src, spl, out=out)
+    torch.cuda.synchronize()
+    # validation: a permutation, and segment i lies in [spl[i-1], spl[i]]
+    ok = fingerprint(out, kb) == fingerprint(src, kb)
+    sdt = torch.int64 if kb == 8 else torch.int32
+    w = out.view(sdt) ^ torch.iinfo(sdt).min
+    sp = spl.view(sdt) ^ torch.iinfo(sdt).min
+    ends = torch.cumsum(counts, 0).tolist()
+    b0 = 0
+    for i, e in enumerate(ends):
+        if e > b0:
+            seg = w[b0:e]
+            if i > 0:
+                ok = ok and bool((seg >= sp[i - 1]).all())
+            if i < len(ends) - 1:
+                ok = ok and bool((seg <= sp[i]).all())
+        b0 = e
+    times = []
+    for _ in range(steps + 2):
+        torch.cuda.synchronize()
+        a_ = torch.cuda.Event(enable_timing=True)
+        b_ = torch.cuda.Event(enable_timing=True)
+        a_.record()
+        vx.partition(src, spl, out=out)
+        b_.record()
+        torch.cuda.synchronize()
+        times.append(a_.elapsed_time(b_))
+    ms = statistics.mean(times[2:])
+    res = {"n": n, "key_type": kt, "splitters": 255, "ms": round(ms, 4),
+           "gb_per_s": round(n * kb / (ms * 1e-3) / 1e9, 2),
+           "hbm_frac": round(3 * n * kb / (ms * 1e-3) / 1e9 / peak, 4), "validated": bool(ok)}
+    try:  # the reference's own partition bench (2-way, median pivot; largest size it runs)
+        import ctypes
+        import oracle
+        if oracle.ref_available():
+            ns = (ctypes.c_size_t * 16)()
+            mb = (ctypes.c_double * 16)()
+            k = oracle.ref().ref_partition_bench(6 if kt == "u64" else 3, 1 << 24, 3, 1, ns, mb, 16)
+            if k > 0:
+                res["reference_cpu_1core"] = {"n": int(ns[k - 1]), "gb_per_s": round(mb[k - 1] / 1e3, 3),
+                                              "what": "run_partition_bench (2-way, 1 core), harness.cpp:409-489"}
+    except Exception as e:  # noqa: BLE001
+        res["reference_cpu_1core"] = {"error": str(e)[:200]}
+    del src, out
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_single(args):
     import torch
     import paper_2205_05982_b200 as vx
     from paper_2205_05982_b200 import workloads
     peak, peak_src = measured_peaks()
-    x, kt, desc = workloads.make(args.workload, n=args.n)
+    src, x, kt, desc = load_workload(args.workload, n=args.n)
+    if x is None:
+        x = src.cpu().numpy()
     n = x.shape[0]
     kb = vx.KEY_BYTES[kt]
-    src = to_device(x, kt)
     buf = torch.empty_like(src)
     ws = torch.empty(vx.workspace_bytes(n, kt), dtype=torch.uint8, device="cuda")
     # correctness gate before timing
@@ -398,32 +568,14 @@ def run_single(args):
         for wl in args.extras.split(","):
             if not wl or wl == args.workload:
                 continue
-            xe, kte, de = workloads.make(wl)
-            ne = xe.shape[0]
-            se = to_device(xe, kte)
-            be = torch.empty_like(se)
-            wse = torch.empty(vx.workspace_bytes(ne, kte), dtype=torch.uint8, device="cuda")
-            be.copy_(se)
-            vx.sort(be, vx.SortConfig(order=vx.Order(int(de)), seed=1),
-                    key_type=kte if kte in ("k128", "kv64") else None, workspace=wse)
-            torch.cuda.synchronize()
-            okx = check_sorted_device(be, kte, de, se)
-            te, _, ste, _ = gpu_time_sorts(be, se, wse, kte, de, 3, 2)
-            _, _, _, pre = gpu_time_sorts(be, se, wse, kte, de, 3, 1, profile=True)
-            mse = statistics.mean(te)
-            kbe = vx.KEY_BYTES[kte]
-            pe = roofline(pre, ste, ne, kbe, peak)
-            sc = pe.get("k_scatter")
-            extra[wl] = {"mkeys_s": round(ne / (mse * 1e-3) / 1e6, 2), "ms": round(mse, 3), "n": ne,
-                         "gb_per_s_sorted": round(ne * kbe / (mse * 1e-3) / 1e9, 2), "validated": okx,
-                         "levels": ste.max_depth,
-                         "design_hbm_frac": round(algorithmic_bytes(ste, ne, kbe)["total"] / (mse * 1e-3) / 1e9
-                                                  / peak, 4),
-                         "scatter_frac": (round(sc["bytes_per_sort"] / (sc["ms"] / 3 * 1e-3) / 1e9 / peak, 4)
-                                          if sc else None),
-                         "kernels_ms": {k: round(v[1] / 3, 4) for k, v in pre.items()}}
-            del se, be, wse
-            torch.cuda.empty_cache()
+            try:
+                if wl.startswith("partition-"):
+                    extra[wl] = time_partition(wl.split("-")[1], peak)
+                else:
+                    extra[wl] = time_extra(wl, peak)
+            except Exception as e:  # noqa: BLE001  (an extra never hides the headline)
+                extra[wl] = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
+                log(f"extra {wl} failed: {e}")
         line["extra"] = extra
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(x, kt, desc)
@@ -431,93 +583,222 @@ def run_single(args):
 
 
 def run_reference(args):
+    """The reference's own CPU sort on this host, same config as the GPU arm:
+    each step is the harness's threads mode (harness.cpp:316-358) -- every
+    host core sorts its own full-size copy of the workload with
+    vexsort::sort -- and value = cores * n / step wall time."""
     from paper_2205_05982_b200 import workloads
-    x, kt, desc = workloads.make(args.workload, n=args.n)
-    cores = os.cpu_count() or 1
-    n_each = min(KEYS_PER_CPU_INSTANCE, x.shape[0])
-    cpu_reference_run(x, kt, desc, cores, n_each, reps=max(1, args.warmup))
-    times, kind = cpu_reference_run(x, kt, desc, cores, n_each, reps=args.steps)
+    name = args.workload or DEFAULT_SINGLE
+    x, kt, desc = workloads.make(name, n=args.n)
+    n = int(x.shape[0])
+    cores = max_instances(x)
+    cpu_instances(x, kt, desc, cores, max(1, args.warmup))
+    times, kind = cpu_instances(x, kt, desc, cores, args.steps)
     t = statistics.mean(times)
-    val = round(cores * n_each / t / 1e6, 2)
+    val = round(cores * n / t / 1e6, 2)
     return {
         "impl": "reference",
         "metric": "Mkeys/s sorted (in-memory key sort)",
         "value": val, "unit": "Mkeys/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": kt, "data": "synthetic (seeded SplitMix64; BASELINE.json config shapes)",
-        "config": {"workload": args.workload, "n": int(x.shape[0]), "key_type": kt,
-                   "order": "desc" if desc else "asc", "parallelism": f"{cores} host threads"},
-        "cpu_baseline": {"value": val, "unit": "Mkeys/s", "cores": cores, "kind": kind,
-                         "sample": f"each step: {cores} independent vexsort::sort instances x {n_each} keys "
-                                   f"of the workload (harness threads mode, harness.cpp:316-358)"},
+        "config": {"workload": name, "n": n, "key_type": kt, "order": "desc" if desc else "asc",
+                   "parallelism": f"{cores} host threads (independent instances, full-size copies)"},
+        "cpu_baseline": {"value": val, "unit": "Mkeys/s", "cores": cores, "kind": kind, "isa": cpu_isa(),
+                         "sample": f"each step: {cores} independent vexsort::sort instances, each on a full-size "
+                                   f"copy of the workload ({n} keys; harness threads mode, "
+                                   f"harness.cpp:316-358); NaN -> +inf (the reference rejects NaN)"},
         "e2e": {"value": val, "unit": "Mkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
-def run_distributed(args):
+NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (B200 nominal; the exchange's bound)
+
+
+def dist_validate(out, src, kt, desc, group):
+    """Global check of a distributed sort, on the devices: (1) each rank's
+    slice is sorted; (2) rank boundaries are ordered (all-gather of every
+    rank's first and last key); (3) the all-reduced multiset fingerprint of
+    the outputs equals that of the inputs (a sorted permutation of integer
+    keys is unique, so (1)-(3) <=> equality with the CPU reference, SURVEY
+    §8c.5)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    kb = KEY_BYTES[kt]
+    ok = check_sorted_device(out, kt, desc)
+    # (2) boundaries: every rank's first and last key (raw words, zero-
+    # extended into int64 lanes), decoded and compared on the host
+    n = out.shape[0]
+    wpk = 2 if kb == 16 else 1
+    ends = torch.zeros(1 + 2 * wpk, dtype=torch.int64, device=out.device)
+    if n:
+        if kb >= 8:
+            w = out.reshape(-1).view(torch.int64)
+        else:
+            w = out.reshape(-1).view({2: torch.int16, 4: torch.int32}[kb]).to(torch.int64) & ((1 << (8 * kb)) - 1)
+        ends[0] = 1
+        ends[1:1 + wpk] = w[:wpk]
+        ends[1 + wpk:] = w[w.numel() - wpk:]
+    allends = torch.empty(world * ends.numel(), dtype=torch.int64, device=out.device)
+    dist.all_gather_into_tensor(allends, ends, group=group)
+    e = allends.view(world, -1).cpu().numpy()
+    npdt = {"i16": np.int16, "u16": np.uint16, "i32": np.int32, "u32": np.uint32, "f32": np.float32,
+            "i64": np.int64, "u64": np.uint64, "f64": np.float64}
+
+    def key(words):  # canonical order key (SURVEY §8c): NaN after everything, -0.0 < +0.0
+        if kb == 16:
+            u = words.astype(np.int64).view(np.uint64)
+            return (int(u[1]), int(u[0]))
+        v = words[:1].astype(np.int64).view(np.uint64).astype({2: np.uint16, 4: np.uint32, 8: np.uint64}[kb])
+        v = v.view(npdt[kt])[0]
+        if kt in ("f32", "f64"):
+            return (1, 0.0, 0) if np.isnan(v) else (0, float(v), int(np.signbit(v) == 0))
+        return int(v)
+
+    prev = None
+    for r in range(world):
+        if not e[r][0]:
+            continue
+        first, last = key(e[r][1:1 + wpk]), key(e[r][1 + wpk:])
+        if prev is not None:
+            if kt in ("f32", "f64") and desc:  # NaN still last; the rest descending
+                ok = ok and (prev[0] < first[0] or (prev[0] == first[0] == 0 and prev[1:] >= first[1:])
+                             or prev[0] == first[0] == 1)
+            else:
+                ok = ok and ((prev >= first) if desc else (prev <= first))
+        prev = last
+    # (3) multiset: sums (wrapping int64) of the mixed keys, inputs vs outputs
+    fi = fingerprint(src, kb)
+    fo = fingerprint(out, kb) if n else (0, 0)
+    to_i64 = lambda v: ((v + 2 ** 63) % 2 ** 64) - 2 ** 63  # noqa: E731
+    t = torch.tensor([to_i64(fi[0]), to_i64(fi[1]), src.shape[0], to_i64(fo[0]), to_i64(fo[1]), n],
+                     dtype=torch.int64, device=out.device)
+    dist.all_reduce(t, group=group)
+    t = t.tolist()
+    ok = ok and t[0] == t[3] and t[1] == t[4] and t[2] == t[5]
+    okt = torch.tensor([1 if ok else 0], device=out.device)
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN, group=group)
+    return bool(int(okt))
+
+
+def dist_steps(src, order, kt, exchange, steps, warmup, group, profile=False):
+    """Timed distributed sorts: barrier + synchronize on both sides of each
+    step, CUDA events on the launching stream, max over ranks."""
     import torch
     import torch.distributed as dist
     import paper_2205_05982_b200 as vx
-    from paper_2205_05982_b200 import workloads
+    from paper_2205_05982_b200.dist import dist_sort
+    stream = torch.cuda.current_stream()
+    tm = {}
+    out = None
+    for _ in range(warmup):
+        out = dist_sort(src, order=order, key_type=kt, exchange=exchange, copy_out=False, group=group)
+    torch.cuda.synchronize()
+    if profile:
+        vx.profile_reset()
+        vx.profile_enable(True)
+    times = []
+    for _ in range(steps):
+        dist.barrier(group=group)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        out = dist_sort(src, order=order, key_type=kt, exchange=exchange, copy_out=False, group=group,
+                        timings=tm)
+        b.record(stream)
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+    prof = None
+    if profile:
+        prof = vx.profile_read()
+        vx.profile_enable(False)
+    t = torch.tensor([statistics.mean(times)], device=src.device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t), out, tm, prof
+
+
+def run_distributed(args):
+    """Distributed sample sort, one rank per GPU.  Default
+    workload: BASELINE configs[4] (C5) -- u64, 2^30 uniform keys per rank
+    (weak scaling), with the u^4-skewed variant as an extra; rank r's keys
+    come from its own seeded stream."""
+    import torch
+    import torch.distributed as dist
+    import paper_2205_05982_b200 as vx
     from paper_2205_05982_b200.dist import dist_sort
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ndev = torch.cuda.device_count()
+    if args.dist_backend == "gloo":
+        # debug mode: ranks may share one GPU (all collectives over gloo with
+        # CUDA tensors; the fused exchange still maps peers' IPC windows)
+        torch.cuda.set_device(local % ndev)
+        dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peak, _ = measured_peaks()
-    x, kt, desc = workloads.make(args.workload, n=args.n, seed=1 + rank)
-    n = x.shape[0]
-    kb = vx.KEY_BYTES[kt]
-    src = to_device(x, kt)
+    name = args.workload or DEFAULT_DIST
+    src, _, kt, desc = load_workload(name, n=args.n, rank=rank)
+    n = int(src.shape[0])
+    kb = KEY_BYTES[kt]
     order = vx.Order(int(desc))
-    for _ in range(args.warmup):
-        out = dist_sort(src, order=order, key_type=kt, exchange=args.exchange, copy_out=False)
-    torch.cuda.synchronize()
-    # validation: local sortedness + boundary monotonicity + global count
-    ok = check_sorted_device(out, kt, desc)
-    cnt = torch.tensor([out.shape[0]], device="cuda", dtype=torch.int64)
-    dist.all_reduce(cnt)
-    ok = ok and int(cnt) == n * world
-    times = []
-    stream = torch.cuda.current_stream()
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            dist.barrier()
-            torch.cuda.synchronize()
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            out = dist_sort(src, order=order, key_type=kt, exchange=args.exchange, copy_out=False)
-            b.record(stream)
-            torch.cuda.synchronize()
-            times.append(a.elapsed_time(b))
-    t = torch.tensor([statistics.mean(times)], device="cuda", dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    okt = torch.tensor([1 if ok else 0], device="cuda")
-    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
-    ms = float(t)
-    # one untimed profiled step: our kernel launches per step + dominant-kernel roofline
-    dist.barrier()
-    vx.profile_reset()
-    vx.profile_enable(True)
     out = dist_sort(src, order=order, key_type=kt, exchange=args.exchange, copy_out=False)
     torch.cuda.synchronize()
-    prof = vx.profile_read()
-    vx.profile_enable(False)
+    ok = dist_validate(out, src, kt, desc, None)
+    with ClockSampler(local % max(1, ndev)) as clk:
+        ms, out, tm, _ = dist_steps(src, order, kt, args.exchange, args.steps, args.warmup, None)
+    recv = torch.tensor([int(out.shape[0])], device="cuda", dtype=torch.float64)
+    allrecv = torch.empty(world, device="cuda", dtype=torch.float64)
+    dist.all_gather_into_tensor(allrecv, recv)
+    allrecv = allrecv.tolist()
+    imbalance = max(allrecv) / (sum(allrecv) / world)
+    # one untimed profiled step: launches per step, the exchange kernel vs NVLink
+    _, _, tmp, prof = dist_steps(src, order, kt, args.exchange, 1, 0, None, profile=True)
     launches = sum(v[0] for v in prof.values())
-    sc = [(l, m) for k, (l, m) in prof.items() if k.split("@")[0] == "k_scatter"]
-    sc_l, sc_ms = sum(l for l, _ in sc), sum(m for _, m in sc)
-    achieved = (2 * n * kb) / ((sc_ms / max(sc_l, 1)) * 1e-3) / 1e9 if sc_l else 0.0
-    ach = torch.tensor([achieved], device="cuda", dtype=torch.float64)
-    dist.all_reduce(ach, op=dist.ReduceOp.MIN)
-    # e2e through the public API at N GPUs: pinned host keys -> H2D -> dist_sort -> D2H, max over ranks
+    sent_remote = (n - int(tmp["send_counts"][rank])) * kb if "send_counts" in tmp else 0
+    kp = prof.get("k_part")
+    xt = torch.tensor([kp[1] / kp[0] if kp else 0.0, sent_remote], device="cuda", dtype=torch.float64)
+    allxt = torch.empty(2 * world, device="cuda", dtype=torch.float64)
+    dist.all_gather_into_tensor(allxt, xt)
+    allxt = allxt.view(world, 2).tolist()
+    x_ms = max(r[0] for r in allxt)
+    x_bytes = max(r[1] for r in allxt)
+    x_ach = x_bytes / (x_ms * 1e-3) / 1e9 if x_ms > 0 else 0.0
+    # extras: the skewed variant, and the NCCL all-to-all exchange baseline
+    extra = {}
+    if not args.no_extras:
+        for wl, exch in (("c5-skew", args.exchange), (name, "nccl")):
+            key = wl if exch == args.exchange else f"{wl}+exchange_nccl"
+            try:
+                se, _, kte, de = load_workload(wl, n=args.n, rank=rank)
+                oe = dist_sort(se, order=vx.Order(int(de)), key_type=kte, exchange=exch, copy_out=False)
+                torch.cuda.synchronize()
+                oke = dist_validate(oe, se, kte, de, None)
+                mse, oe, _, _ = dist_steps(se, vx.Order(int(de)), kte, exch, 3, 1, None)
+                r_ = torch.tensor([float(oe.shape[0])], device="cuda", dtype=torch.float64)
+                ar = torch.empty(world, device="cuda", dtype=torch.float64)
+                dist.all_gather_into_tensor(ar, r_)
+                ar = ar.tolist()
+                extra[key] = {"ms": round(mse, 3), "mkeys_s": round(world * se.shape[0] / (mse * 1e-3) / 1e6, 2),
+                              "validated": oke, "imbalance": round(max(ar) / (sum(ar) / world), 4),
+                              "exchange": exch}
+                del se, oe
+            except Exception as e:  # noqa: BLE001
+                extra[key] = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
+            torch.cuda.empty_cache()
+    # e2e through the public API at N GPUs: pinned host keys -> H2D -> dist_sort -> D2H (max over ranks)
+    stream = torch.cuda.current_stream()
     host = torch.empty(src.shape, dtype=src.dtype).pin_memory()
-    host.copy_(src.cpu())
+    host.copy_(src)
     dev_in = torch.empty_like(src)
-    host_out = torch.empty((2 * n,) + tuple(src.shape[1:]), dtype=src.dtype).pin_memory()
+    cap = int(max(allrecv) * 1.1) + 1024
+    host_out = torch.empty((cap,) + tuple(src.shape[1:]), dtype=src.dtype).pin_memory()
     e2e_times, d2h_bytes = [], 0
-    for _ in range(min(args.steps, 5)):
+    for _ in range(max(1, min(args.steps, 3))):
         dist.barrier()
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True)
@@ -541,21 +822,31 @@ def run_distributed(args):
             "value": round(world * n / (ms * 1e-3) / 1e6, 2), "unit": "Mkeys/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": kt,
-            "data": "synthetic (seeded SplitMix64 per rank; BASELINE.json config shapes)",
-            "config": {"workload": args.workload + " (per rank)", "n_per_rank": n, "key_type": kt,
-                       "parallelism": f"distributed sample sort x{world} (NCCL all-gather of samples/counts; "
-                                              f"{args.exchange} key exchange)"},
-            "validated": bool(int(okt)),
+            "data": "synthetic (seeded SplitMix64 per rank, generated on the device; BASELINE.json configs[4])",
+            "config": {"workload": name + " (per rank)", "n_per_rank": n, "key_type": kt,
+                       "order": "desc" if desc else "asc",
+                       "parallelism": f"distributed sample sort x{world} ({args.dist_backend}: all-gather of "
+                                      f"samples / counts; {args.exchange} key exchange)",
+                       "l2": f"inputs ({n * kb / 1e9:.1f} GB per rank) far larger than L2 (126 MB)"},
+            "validated": ok,
+            "validation": "per-rank sortedness + rank-boundary order + all-reduced multiset fingerprint",
+            "imbalance": round(imbalance, 4),
+            "recv_keys_per_rank": [int(v) for v in allrecv],
             "gb_per_s_sorted": round(world * n * kb / (ms * 1e-3) / 1e9, 2),
             "clocks": clk.summary(),
-            "peak_hbm_gbs": peak,
-            "roofline": {"bound": "hbm", "kernel": "k_scatter", "achieved": round(float(ach), 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(float(ach) / peak, 4) if peak else None, "traffic": None,
-                         "note": "min over ranks; 2*n_local*key_bytes per launch / mean launch time"},
+            "roofline": {"bound": "nvlink", "kernel": "k_part (fused partition + peer stores)",
+                         "achieved": round(x_ach, 1), "peak": NVLINK_GBS, "unit": "GB/s",
+                         "frac": round(x_ach / NVLINK_GBS, 4), "traffic": None,
+                         "algorithmic_bytes_per_launch": int(x_bytes), "avg_launch_ms": round(x_ms, 4),
+                         "note": "keys stored into peer windows ((G-1)/G of the local keys) / k_part time, "
+                                 "max over ranks; peak = NVLink 5 per direction (nominal)",
+                         "hbm_peak": peak},
             "e2e": {"value": round(world * n / (e2e_ms * 1e-3) / 1e6, 2), "unit": "Mkeys/s",
                     "h2d_bytes_per_step": n * kb, "d2h_bytes_per_step": d2h_bytes, "ms_per_step": round(e2e_ms, 3),
                     "api": "pinned host keys per rank -> H2D -> dist_sort -> D2H (max over ranks)"},
             "gpu_launches": int(launches) * args.steps,
+            "kernels_ms_rank0": {k: round(v[1], 4) for k, v in prof.items()},
+            "extra": extra,
         }
     dist.destroy_process_group()
     return line
@@ -567,9 +858,12 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="c2-u32-asc")
+    ap.add_argument("--workload", default=None,
+                    help=f"default {DEFAULT_SINGLE} on one GPU, {DEFAULT_DIST} (per rank) distributed")
     ap.add_argument("--n", type=int, default=None)
-    ap.add_argument("--extras", default="u64-uniform,c2-f32-asc")
+    ap.add_argument("--extras", default=DEFAULT_EXTRAS)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: debug mode, ranks may share one GPU (collectives over gloo)")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-API e2e leg (ncu launch lists only)")
@@ -589,6 +883,7 @@ def main():
         if line is not None:
             print(json.dumps(line), flush=True)
         return
+    args.workload = args.workload or DEFAULT_SINGLE
     print(json.dumps(run_single(args)), flush=True)
 
 

@@ -85,11 +85,33 @@ def ref_available() -> bool:
     return os.path.exists(os.path.join(_HERE, "_ref", "libvexsort_ref.so"))
 
 
+def host_has_avx512vl_dq() -> bool:
+    """The reference's ISA probe (CMakeLists.txt:34-65): AVX-512VL + DQ."""
+    try:
+        flags = open("/proc/cpuinfo").read()
+    except OSError:
+        return False
+    return all(f" {f}" in flags for f in ("avx512f", "avx512vl", "avx512dq"))
+
+
+def ref_path() -> str:
+    """The reference build this host would get from its own CMake: the
+    AVX-512VL/DQ variant when the CPU has it, else the AVX2 build."""
+    wide = os.path.join(_HERE, "_ref", "libvexsort_ref_avx512.so")
+    if os.environ.get("VXSORT_REF_ISA", "auto") != "avx2" and os.path.exists(wide) and host_has_avx512vl_dq():
+        return wide
+    return os.path.join(_HERE, "_ref", "libvexsort_ref.so")
+
+
 def ref():
     """The real reference (compiled from /root/reference sources)."""
     global _ref
     if _ref is None:
-        _ref = _load(os.path.join(_HERE, "_ref", "libvexsort_ref.so"))
+        _ref = _load(ref_path())
+        _ref.ref_isa.restype = ctypes.c_char_p
+        _ref.ref_partition_bench.argtypes = [ctypes.c_int, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64,
+                                             ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_double),
+                                             ctypes.c_int]
         _ref.ref_sort.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
                                   ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(Stats)]
         _ref.ref_sort_instances.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_size_t,

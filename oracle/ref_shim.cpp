@@ -10,6 +10,7 @@
 //   Driver::heap_sort / depth_budget          driver.hpp:38-41, 96-121
 //   PivotSampler::choose_pivot, Sfc64         pivot.hpp:25-172
 //   vexbench::generate<T>                     harness.cpp:179-219
+//   vexbench::run_partition_bench             harness.cpp:409-489
 #include <atomic>
 #include <cstdint>
 #include <cstring>
@@ -189,6 +190,44 @@ int ref_generate(void* out, std::size_t n, int type, int dist, std::uint64_t see
     std::memcpy(out, v.data(), n * sizeof(T));
     return 0;
   });
+}
+
+// The reference's own partition-only benchmark (harness.cpp:409-489: 2-way
+// Partitioner::partition with a median pivot, verified every rep), at sizes
+// 2^10 .. max_n in powers of four.  Fills up to cap (n, median MB/s) pairs;
+// returns how many, or -1 on a verification failure.
+int ref_partition_bench(int type, std::size_t max_n, std::size_t reps, std::uint64_t seed,
+                        std::size_t* n_out, double* mbps_out, int cap) {
+  try {
+    vexbench::PartitionBenchConfig cfg;
+    cfg.type = static_cast<vexbench::KeyType>(type);
+    cfg.max_n = max_n;
+    cfg.reps = reps;
+    cfg.seed = seed;
+    const auto res = vexbench::run_partition_bench(cfg);
+    int k = 0;
+    for (const auto& r : res) {
+      if (k >= cap) break;
+      n_out[k] = r.n;
+      mbps_out[k] = r.mbps_median;
+      ++k;
+    }
+    return k;
+  } catch (const std::exception& e) {
+    std::snprintf(g_err, sizeof(g_err), "%s", e.what());
+    return -1;
+  }
+}
+
+// ISA the shim was compiled for (the reference's wide backend follows it).
+const char* ref_isa() {
+#if defined(__AVX512VL__) && defined(__AVX512DQ__)
+  return "avx2+avx512vl/dq";
+#elif defined(__AVX2__)
+  return "avx2";
+#else
+  return "scalar";
+#endif
 }
 
 }  // extern "C"

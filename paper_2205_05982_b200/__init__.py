@@ -220,16 +220,41 @@ def infer_key_type(keys, key_type: Optional[str] = None) -> str:
 
 def _nkeys(keys, key_type):
     if key_type in ("k128", "kv64"):
-        if tuple(keys.shape[1:]) != (2,):
+        if keys.ndim != 2 or tuple(keys.shape[1:]) != (2,):
             raise ValueError("K128/KV64 keys must have shape (n, 2) of 64-bit words {lo, hi}")
         return int(keys.shape[0])
-    return int(keys.shape[0]) if keys.ndim else 1
+    if keys.ndim != 1:
+        raise ValueError(f"{key_type} keys must be a 1-D array (got shape {tuple(keys.shape)})")
+    return int(keys.shape[0])
+
+
+def _device_of(t):
+    """torch.cuda.device context for a CUDA tensor: kernels launch on the
+    tensor's device and that device's current stream."""
+    import torch
+    return torch.cuda.device(t.device)
+
+
+def _check_cuda(t, what="keys"):
+    if not (_is_torch(t) and t.is_cuda):
+        raise ValueError(f"{what} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
 
 
 def workspace_bytes(n: int, key_type: str) -> int:
     out = ctypes.c_size_t()
     _check(lib().vxs_sort_workspace_bytes(n, KEY_CODE[key_type], ctypes.byref(out)))
     return out.value
+
+
+def _ws_args(workspace, keys):
+    if workspace is None:
+        return None, 0
+    _check_cuda(workspace, "workspace")
+    if workspace.device != keys.device:
+        raise ValueError("workspace must live on the keys' device")
+    return workspace.data_ptr(), workspace.numel() * workspace.element_size()
 
 
 def _stream_ptr(stream):
@@ -255,11 +280,10 @@ def sort(keys, config: Optional[SortConfig] = None, key_type: Optional[str] = No
             raise ValueError("torch tensors must live on a CUDA device (use numpy for host arrays)")
         if not keys.is_contiguous():
             raise ValueError("keys must be contiguous")
-        ws_ptr, ws_n = (None, 0)
-        if workspace is not None:
-            ws_ptr, ws_n = workspace.data_ptr(), workspace.numel() * workspace.element_size()
-        _check(lib().vxs_sort(keys.data_ptr(), n, KEY_CODE[kt], int(cfg.order), seed, has_seed,
-                              ws_ptr, ws_n, _stream_ptr(stream), ctypes.byref(st)))
+        ws_ptr, ws_n = _ws_args(workspace, keys)
+        with _device_of(keys):
+            _check(lib().vxs_sort(keys.data_ptr(), n, KEY_CODE[kt], int(cfg.order), seed, has_seed,
+                                  ws_ptr, ws_n, _stream_ptr(stream), ctypes.byref(st)))
         return st
     arr = keys
     if not isinstance(arr, np.ndarray) or not arr.flags.c_contiguous or not arr.flags.writeable:
@@ -276,15 +300,14 @@ def sort_range(keys, lo: int, hi: int, config: Optional[SortConfig] = None, key_
     keys[:lo] precede them and keys[hi:] follow them (unordered)."""
     cfg = config or SortConfig()
     kt = infer_key_type(keys, key_type)
-    if not (_is_torch(keys) and keys.is_cuda and keys.is_contiguous()):
-        raise ValueError("sort_range takes a contiguous CUDA tensor")
+    _check_cuda(keys)
     n = _nkeys(keys, kt)
-    ws_ptr, ws_n = (None, 0) if workspace is None else (workspace.data_ptr(),
-                                                       workspace.numel() * workspace.element_size())
+    ws_ptr, ws_n = _ws_args(workspace, keys)
     sd, has = _seed_args(cfg.seed)
     st = SortStats()
-    _check(lib().vxs_sort_range(keys.data_ptr(), n, KEY_CODE[kt], int(cfg.order), int(lo), int(hi), sd, has,
-                                ws_ptr, ws_n, _stream_ptr(stream), ctypes.byref(st)))
+    with _device_of(keys):
+        _check(lib().vxs_sort_range(keys.data_ptr(), n, KEY_CODE[kt], int(cfg.order), int(lo), int(hi), sd, has,
+                                    ws_ptr, ws_n, _stream_ptr(stream), ctypes.byref(st)))
     return st
 
 
@@ -325,17 +348,21 @@ def argsort(keys, order: Order = Order.kAscending, key_type: Optional[str] = Non
     writes the sorted keys into ``sorted_keys``.  ``keys`` is not modified."""
     import torch
     kt = infer_key_type(keys, key_type)
-    if not (_is_torch(keys) and keys.is_cuda and keys.is_contiguous()):
-        raise ValueError("argsort takes a contiguous CUDA tensor")
+    _check_cuda(keys)
     n = _nkeys(keys, kt)
+    if sorted_keys is not None:
+        _check_cuda(sorted_keys, "sorted_keys")
+        if (sorted_keys.dtype != keys.dtype or sorted_keys.numel() != keys.numel()
+                or sorted_keys.device != keys.device):
+            raise ValueError("sorted_keys must match keys in dtype, size and device")
     idx = torch.empty(n, dtype=torch.int64, device=keys.device)
-    ws_ptr, ws_n = (None, 0) if workspace is None else (workspace.data_ptr(),
-                                                       workspace.numel() * workspace.element_size())
+    ws_ptr, ws_n = _ws_args(workspace, keys)
     sd, has = _seed_args(seed)
     st = SortStats()
-    _check(lib().vxs_argsort(keys.data_ptr(), n, KEY_CODE[kt], int(order), idx.data_ptr(),
-                             None if sorted_keys is None else sorted_keys.data_ptr(), sd, has, ws_ptr, ws_n,
-                             _stream_ptr(stream), ctypes.byref(st)))
+    with _device_of(keys):
+        _check(lib().vxs_argsort(keys.data_ptr(), n, KEY_CODE[kt], int(order), idx.data_ptr(),
+                                 None if sorted_keys is None else sorted_keys.data_ptr(), sd, has, ws_ptr, ws_n,
+                                 _stream_ptr(stream), ctypes.byref(st)))
     return idx
 
 
@@ -345,19 +372,20 @@ def sort_pairs(keys, values, config: Optional[SortConfig] = None, key_type: Opti
     element size of 1/2/4/8/16 bytes per key) alongside, stably (§8 f2)."""
     cfg = config or SortConfig()
     kt = infer_key_type(keys, key_type)
-    for t in (keys, values):
-        if not (_is_torch(t) and t.is_cuda and t.is_contiguous()):
-            raise ValueError("sort_pairs takes contiguous CUDA tensors")
+    _check_cuda(keys)
+    _check_cuda(values, "values")
+    if values.device != keys.device:
+        raise ValueError("values must live on the keys' device")
     n = _nkeys(keys, kt)
-    if values.shape[0] != n:
+    if values.ndim == 0 or values.shape[0] != n:
         raise ValueError("values must have one row per key")
     vb = values.numel() * values.element_size() // max(n, 1) if n else values.element_size()
-    ws_ptr, ws_n = (None, 0) if workspace is None else (workspace.data_ptr(),
-                                                       workspace.numel() * workspace.element_size())
+    ws_ptr, ws_n = _ws_args(workspace, keys)
     sd, has = _seed_args(cfg.seed)
     st = SortStats()
-    _check(lib().vxs_sort_pairs(keys.data_ptr(), values.data_ptr(), vb, n, KEY_CODE[kt], int(cfg.order), sd, has,
-                                ws_ptr, ws_n, _stream_ptr(stream), ctypes.byref(st)))
+    with _device_of(keys):
+        _check(lib().vxs_sort_pairs(keys.data_ptr(), values.data_ptr(), vb, n, KEY_CODE[kt], int(cfg.order), sd,
+                                    has, ws_ptr, ws_n, _stream_ptr(stream), ctypes.byref(st)))
     return st
 
 
@@ -369,8 +397,9 @@ def sample(keys, s: int, order: Order = Order.kAscending, seed: int = 1, key_typ
     shape = (s, 2) if KEY_BYTES[kt] == 16 else (s,)
     wdt = {2: torch.uint16, 4: torch.uint32, 8: torch.uint64, 16: torch.uint64}[KEY_BYTES[kt]]
     out = torch.empty(shape, dtype=wdt, device=keys.device)
-    _check(lib().vxs_sample(keys.data_ptr(), n, KEY_CODE[kt], int(order), seed, out.data_ptr(), s,
-                            _stream_ptr(stream)))
+    with _device_of(keys):
+        _check(lib().vxs_sample(keys.data_ptr(), n, KEY_CODE[kt], int(order), seed, out.data_ptr(), s,
+                                _stream_ptr(stream)))
     return out
 
 
@@ -384,9 +413,10 @@ def partition(keys, splitters, order: Order = Order.kAscending, key_type=None, o
     if out is None:
         out = torch.empty_like(keys)
     counts = torch.zeros(nspl + 1, dtype=torch.int64, device=keys.device)
-    _check(lib().vxs_partition(keys.data_ptr(), n, KEY_CODE[kt], int(order),
-                               splitters.data_ptr() if nspl else None, nspl, out.data_ptr(),
-                               counts.data_ptr(), None, 0, _stream_ptr(stream)))
+    with _device_of(keys):
+        _check(lib().vxs_partition(keys.data_ptr(), n, KEY_CODE[kt], int(order),
+                                   splitters.data_ptr() if nspl else None, nspl, out.data_ptr(),
+                                   counts.data_ptr(), None, 0, _stream_ptr(stream)))
     return out, counts
 
 
@@ -399,9 +429,10 @@ def partition_counts(keys, splitters, workspace, order: Order = Order.kAscending
     n = _nkeys(keys, kt)
     nspl = int(splitters.shape[0])
     counts = torch.zeros(nspl + 1, dtype=torch.int64, device=keys.device)
-    _check(lib().vxs_partition_counts(keys.data_ptr(), n, KEY_CODE[kt], int(order),
-                                      splitters.data_ptr() if nspl else None, nspl, counts.data_ptr(),
-                                      workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)))
+    with _device_of(keys):
+        _check(lib().vxs_partition_counts(keys.data_ptr(), n, KEY_CODE[kt], int(order),
+                                          splitters.data_ptr() if nspl else None, nspl, counts.data_ptr(),
+                                          workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)))
     return counts
 
 
@@ -411,9 +442,10 @@ def partition_exchange(keys, nspl: int, dst_addrs, dst_offsets, workspace, order
     stored at element dst_offsets[i] of the buffer at address dst_addrs[i]
     (int64 device tensors of nspl+1 entries; peers' receive buffers)."""
     kt = infer_key_type(keys, key_type)
-    _check(lib().vxs_partition_exchange(keys.data_ptr(), _nkeys(keys, kt), KEY_CODE[kt], int(order), int(nspl),
-                                        dst_addrs.data_ptr(), dst_offsets.data_ptr(), workspace.data_ptr(),
-                                        workspace.numel(), _stream_ptr(stream)))
+    with _device_of(keys):
+        _check(lib().vxs_partition_exchange(keys.data_ptr(), _nkeys(keys, kt), KEY_CODE[kt], int(order),
+                                            int(nspl), dst_addrs.data_ptr(), dst_offsets.data_ptr(),
+                                            workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)))
 
 
 class DeviceBlock:
@@ -460,8 +492,10 @@ class DeviceBlock:
 def transform(keys, order: Order = Order.kAscending, inverse=False, key_type=None, stream=None):
     """Apply the order-preserving key transform in place (device keys)."""
     kt = infer_key_type(keys, key_type)
-    _check(lib().vxs_transform(keys.data_ptr(), _nkeys(keys, kt), KEY_CODE[kt], int(order),
-                               int(bool(inverse)), _stream_ptr(stream)))
+    _check_cuda(keys)
+    with _device_of(keys):
+        _check(lib().vxs_transform(keys.data_ptr(), _nkeys(keys, kt), KEY_CODE[kt], int(order),
+                                   int(bool(inverse)), _stream_ptr(stream)))
 
 
 def base_case_capacity(key_type: str) -> int:

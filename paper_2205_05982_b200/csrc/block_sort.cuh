@@ -62,7 +62,6 @@ __device__ __forceinline__ void warp_bitonic_merge(W (&k)[N], int lane) {
     for (int stride = size >> 2; stride > 0; stride >>= 1) {
       if (stride >= N) {
         const int lx = stride / N;
-#pragma unroll
         const bool lower = (lane & lx) == 0;
 #pragma unroll
         for (int i = 0; i < N; ++i) k[i] = keep_minmax(k[i], shfl_xor(k[i], lx), lower);
@@ -317,225 +316,25 @@ __device__ __forceinline__ void block_minmax(const W (&k)[ITEMS], W& lo, W& hi, 
 }
 
 // k[]: keys striped (key i*THREADS + tid), transformed domain, padded
-// beyond `size` with a copy of one of the item's keys (neutral for min/max).  Writes the sorted, decoded item to dst and returns
-// true, or returns false (nothing written, k[] untouched) when the bins are
-// too unbalanced.  smem: BinSort<W,THREADS,ITEMS>::kSmem bytes.
-// Rank variant (8-byte keys, measured faster for them): one returning atomic
-// per key in the counting pass yields its rank inside the bin; the scatter
-// pass is prefix + rank.  Same contract as bin_sort_item.
-template <typename W, int THREADS, int ITEMS, bool FLT>
-__device__ __forceinline__ bool bin_sort_item_rank(const W (&k)[ITEMS], int size, unsigned char* smem, W* dst,
-                                              const Xf<W>& X) {
+// beyond `size` with a copy of one of the item's keys (neutral for min/max).
+// Writes the sorted, decoded item to dst and returns true, or returns false
+// (nothing written, k[] untouched) when the bins are too unbalanced.
+// smem: BinSort<W,THREADS,ITEMS>::kSmem bytes.
+// RANK (8-byte keys, measured faster for them): the counting pass uses a
+// returning atomic, so each key knows its rank inside its bin and the
+// scatter pass is prefix + rank (cnt then keeps bin STARTS).  Otherwise the
+// counting atomics are fire-and-forget and the scatter pass takes slots with
+// a returning atomic on the prefix (cnt then ends as bin ENDS).
+template <typename W, int THREADS, int ITEMS, bool FLT, bool RANK>
+__device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, W* dst, const Xf<W>& X) {
   using BS = BinSort<W, THREADS, ITEMS>;
   constexpr int TOTAL = BS::kTotal;
   constexpr int NB = BS::kNB;
-  constexpr int BPT = BS::kBPT;
   constexpr int NW = THREADS / 32;
   constexpr int NV = ITEMS * (int)sizeof(W) / 16;  // uint4 per thread row
   static_assert(NV * 16 == ITEMS * (int)sizeof(W), "vector rows");
-  // (the dynamic smem is named here, not through the generic `smem`
-  // pointer, so every access is a plain LDS/STS off a shared-window symbol)
-  (void)smem;
-  extern __shared__ __align__(128) unsigned char bs_dyn_r[];
-  W* sk = reinterpret_cast<W*>(bs_dyn_r);  // keys grouped by bin, then sorted
-  unsigned* cnt = reinterpret_cast<unsigned*>(sk + TOTAL);
-  __shared__ W red_lo[NW];
-  __shared__ W red_hi[NW];
-  __shared__ unsigned s_tot[NW];
-  __shared__ unsigned s_sq[NW];
-  __shared__ unsigned s_mx[NW];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int j = tid; j < BS::kCnt / 4; j += THREADS) reinterpret_cast<uint4*>(cnt)[j] = make_uint4(0, 0, 0, 0);
-  W lo, hi;
-  block_minmax<W, THREADS, ITEMS>(k, lo, hi, red_lo, red_hi);  // (its barrier covers cnt)
-  const int bl = key_bitlen(key_sub(hi, lo));
-  const int shift = bl > BS::kNBBits ? bl - BS::kNBBits : 0;
-  unsigned br[ITEMS];  // counter word << 17 | half << 16 | rank inside the bin
-  unsigned sq = 0;     // sum over keys of 2*rank + 1 = sum over bins of count^2
-  unsigned mx = 0;     // largest rank
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const bool valid = i * THREADS + tid < size;
-    const unsigned b = valid ? key_shr32(key_sub(k[i], lo), shift) : (unsigned)(NB + BS::kBinsPerWord);
-    unsigned r;
-    if constexpr (BS::kPacked) {
-      const int w = BS::wslot((int)(b >> 1));
-      const unsigned h = (b & 1u) << 4;
-      r = (atomicAdd(&cnt[w], 1u << h) >> h) & 0xFFFFu;
-      br[i] = ((unsigned)w << 17) | ((b & 1u) << 16) | r;
-    } else {
-      const int w = BS::wslot((int)b);
-      r = atomicAdd(&cnt[w], 1u);
-      br[i] = ((unsigned)w << 17) | r;
-    }
-    sq += 2u * r + 1u;
-    mx = valid ? umax(mx, r) : mx;
-  }
-  __syncthreads();
-  // exclusive scan over the bins; thread t owns bins [t*BPT, (t+1)*BPT)
-  uint4* cg = reinterpret_cast<uint4*>(cnt + BS::wslot(tid * BS::kWPT));
-  unsigned sum = 0;
-#pragma unroll
-  for (int j = 0; j < BS::kWPT / 4; ++j) {
-    const uint4 c = cg[j];
-    if constexpr (BS::kPacked)
-      sum += (c.x & 0xFFFFu) + (c.x >> 16) + (c.y & 0xFFFFu) + (c.y >> 16) + (c.z & 0xFFFFu) + (c.z >> 16) +
-             (c.w & 0xFFFFu) + (c.w >> 16);
-    else
-      sum += c.x + c.y + c.z + c.w;
-  }
-  unsigned incl = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    mx = umax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  }
-  if (lane == 31) s_tot[warp] = incl;
-  if (lane == 0) {
-    s_sq[warp] = sq;
-    s_mx[warp] = mx;
-  }
-  __syncthreads();
-  unsigned base = incl - sum, tsq = 0, rounds = 0;
-#pragma unroll
-  for (int w = 0; w < NW; ++w) {
-    base += w < warp ? s_tot[w] : 0u;
-    tsq += s_sq[w];
-    rounds = umax(rounds, s_mx[w]);
-  }
-  rounds += 1;  // largest bin
-  // block-uniform rejection; cnt is no longer read
-  const unsigned pad = (unsigned)(TOTAL - size);  // the dummy bin adds pad^2
-  if (tsq - pad * pad > 4u * (unsigned)size + 256u || rounds > (unsigned)BS::kMaxBin) return false;
-  auto pre = [&](unsigned x) {  // count(s) -> exclusive prefix(es), same packing
-    if constexpr (BS::kPacked) {
-      const unsigned l = base, h = base + (x & 0xFFFFu);
-      base = h + (x >> 16);
-      return l | (h << 16);
-    } else {
-      const unsigned l = base;
-      base += x;
-      return l;
-    }
-  };
-#pragma unroll
-  for (int j = 0; j < BS::kWPT / 4; ++j) {  // (only this thread touches these counters)
-    const uint4 c = cg[j];
-    uint4 o;
-    o.x = pre(c.x);
-    o.y = pre(c.y);
-    o.z = pre(c.z);
-    o.w = pre(c.w);
-    cg[j] = o;
-  }
-  if (tid == THREADS - 1) {
-    cnt[BS::kEnd] = (unsigned)size;
-    cnt[BS::kDummy] = (unsigned)size;  // padding keys go to [size, TOTAL)
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const unsigned s0 = BS::kPacked ? (cnt[br[i] >> 17] >> (((br[i] >> 16) & 1u) << 4)) & 0xFFFFu : cnt[br[i] >> 17];
-    sk[BS::swz((int)(s0 + (br[i] & 0xFFFFu)))] = i * THREADS + tid < size ? k[i] : key_max<W>();
-  }
-  __syncthreads();
-  // odd-even transposition rounds over this thread's row of ITEMS positions
-  W v[ITEMS];
-  {
-    const uint4* row = reinterpret_cast<const uint4*>(sk);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      const uint4 t = row[(tid * NV + q) ^ (tid & BS::kSwz)];
-      memcpy(reinterpret_cast<char*>(v) + 16 * q, &t, 16);
-    }
-  }
-  if (rounds > 1) {
-#pragma unroll 1
-    for (unsigned r = 0; r < rounds; r += 2) {
-#pragma unroll
-      for (int i = 0; i + 1 < ITEMS; i += 2) cas(v[i], v[i + 1]);
-#pragma unroll
-      for (int i = 1; i + 1 < ITEMS; i += 2) cas(v[i], v[i + 1]);
-      const W nx = shfl_next(v[0]);
-      const W pv = shfl_prev(v[ITEMS - 1]);
-      if (lane < 31 && key_lt(nx, v[ITEMS - 1])) v[ITEMS - 1] = nx;
-      if (lane > 0 && key_lt(v[0], pv)) v[0] = pv;
-    }
-  }
-  {
-    uint4* row = reinterpret_cast<uint4*>(sk);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      uint4 t;
-      memcpy(&t, reinterpret_cast<const char*>(v) + 16 * q, 16);
-      row[(tid * NV + q) ^ (tid & BS::kSwz)] = t;
-    }
-  }
-  __syncthreads();
-  if (NW > 1 && rounds > 1 && lane == 0 && warp > 0) {  // bin straddling the boundary before this warp
-    const int p = warp * 32 * ITEMS;
-    if (p < size) {
-      const int b = (int)key_shr32(key_sub(sk[BS::swz(p)], lo), shift);
-      const int s = (int)BS::half(cnt, b), e = (int)BS::half(cnt, b + 1);
-      if (s < p) {
-        for (int a = s + 1; a < e; ++a) {
-          const W x = sk[BS::swz(a)];
-          int q = a;
-          while (q > s && key_lt(x, sk[BS::swz(q - 1)])) {
-            sk[BS::swz(q)] = sk[BS::swz(q - 1)];
-            --q;
-          }
-          sk[BS::swz(q)] = x;
-        }
-      }
-    }
-    __syncwarp(1u);
-  }
-  __syncthreads();
-  // write-out: key i*THREADS + tid; its swizzle term ((i*THREADS + tid) /
-  // ITEMS) & 7 is per-thread constant when THREADS/ITEMS is a multiple of 8,
-  // so the loads take immediate offsets; full rounds carry no bounds test
-  {
-    constexpr int RPI = THREADS / ITEMS;
-    const int nfull = size / THREADS;  // block-uniform
-    const int trow = tid >> BS::kLogItems;
-    // the swizzle only touches bits below 32*KPC <= THREADS, so
-    // (i*THREADS + tid) ^ sw == i*THREADS + (tid ^ sw)
-    const int e0 = tid ^ ((trow & BS::kSwz) << BS::kLogKpc);
-    const int e1 = tid ^ (((RPI + trow) & BS::kSwz) << BS::kLogKpc);
-    W* d = dst + tid;
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      if (i >= nfull) break;
-      const int e = (RPI % 8 == 0 || (i * RPI) % 8 == 0) ? e0
-                    : ((i * RPI) % 8 == RPI % 8 ? e1 : tid ^ (((i * RPI + trow) & BS::kSwz) << BS::kLogKpc));
-      d[i * THREADS] = dec_x<FLT>(sk[i * THREADS + e], X);
-    }
-    const int idx = nfull * THREADS + tid;
-    if (nfull < ITEMS && idx < size) d[nfull * THREADS] = dec_x<FLT>(sk[BS::swz(idx)], X);
-  }
-  __syncthreads();
-  return true;
-}
-
-template <typename W, int THREADS, int ITEMS, bool FLT>
-__device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, unsigned char* smem, W* dst,
-                                              const Xf<W>& X) {
-  using BS = BinSort<W, THREADS, ITEMS>;
-  constexpr int TOTAL = BS::kTotal;
-  constexpr int NB = BS::kNB;
-  constexpr int BPT = BS::kBPT;
-  constexpr int NW = THREADS / 32;
-  constexpr int NV = ITEMS * (int)sizeof(W) / 16;  // uint4 per thread row
-  static_assert(NV * 16 == ITEMS * (int)sizeof(W), "vector rows");
-  // (the dynamic smem is named here, not through the generic `smem`
-  // pointer, so every access is a plain LDS/STS off a shared-window symbol)
-  (void)smem;
+  // (the dynamic smem is named here, not through a generic pointer, so every
+  // access is a plain LDS/STS off a shared-window symbol)
   extern __shared__ __align__(128) unsigned char bs_dyn[];
   W* sk = reinterpret_cast<W*>(bs_dyn);  // keys grouped by bin, then sorted
   unsigned* cnt = reinterpret_cast<unsigned*>(sk + TOTAL);
@@ -550,9 +349,10 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
   block_minmax<W, THREADS, ITEMS>(k, lo, hi, red_lo, red_hi);  // (its barrier covers cnt)
   const int bl = key_bitlen(key_sub(hi, lo));
   const int shift = bl > BS::kNBBits ? bl - BS::kNBBits : 0;
-  // pass 1: count (fire-and-forget shared atomics)
-  unsigned br[ITEMS];  // counter word << 17 | half << 16
-  unsigned sq = 0, mx = 0;  // sum(count^2) (the cost of the rounds) and the largest bin
+  // pass 1: count.  br[i] = counter word << 17 | half << 16 (| rank, RANK)
+  unsigned br[ITEMS];
+  unsigned sq = 0;  // sum over bins of count^2 (the cost of the rounds)
+  unsigned mx = 0;  // largest bin (RANK: largest rank)
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const bool valid = i * THREADS + tid < size;
@@ -560,7 +360,14 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
     const int w = BS::kPacked ? BS::wslot((int)(b >> 1)) : BS::wslot((int)b);
     const unsigned h = BS::kPacked ? (b & 1u) << 4 : 0u;
     br[i] = ((unsigned)w << 17) | ((h >> 4) << 16);
-    atomicAdd(&cnt[w], 1u << h);
+    if constexpr (RANK) {
+      const unsigned r = (atomicAdd(&cnt[w], 1u << h) >> h) & 0xFFFFu;
+      br[i] |= r;
+      sq += 2u * r + 1u;  // sum over keys of 2*rank + 1 = sum over bins of count^2
+      mx = valid ? umax(mx, r) : mx;
+    } else {
+      atomicAdd(&cnt[w], 1u << h);
+    }
   }
   __syncthreads();
   // exclusive scan over the bins; thread t owns bins [t*BPT, (t+1)*BPT)
@@ -570,12 +377,16 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
     if constexpr (BS::kPacked) {
       const unsigned l = x & 0xFFFFu, hh = x >> 16;
       sum += l + hh;
-      sq += l * l + hh * hh;
-      mx = umax(mx, umax(l, hh));
+      if constexpr (!RANK) {
+        sq += l * l + hh * hh;
+        mx = umax(mx, umax(l, hh));
+      }
     } else {
       sum += x;
-      sq += x * x;
-      mx = umax(mx, x);
+      if constexpr (!RANK) {
+        sq += x * x;
+        mx = umax(mx, x);
+      }
     }
   };
 #pragma unroll
@@ -608,7 +419,12 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
   for (int w = 0; w < NW; ++w) {
     base += w < warp ? s_tot[w] : 0u;
     tsq += s_sq[w];
-    rounds = umax(rounds, s_mx[w]);  // largest bin
+    rounds = umax(rounds, s_mx[w]);
+  }
+  if constexpr (RANK) {
+    rounds += 1;  // largest rank + 1 = largest bin
+    const unsigned pad = (unsigned)(TOTAL - size);  // the padding bin adds pad^2
+    tsq -= pad * pad;
   }
   // block-uniform rejection; cnt is no longer read
   if (tsq > 4u * (unsigned)size + 256u || rounds > (unsigned)BS::kMaxBin) return false;
@@ -638,12 +454,13 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
     cnt[BS::kDummy] = (unsigned)size;  // padding keys go to [size, TOTAL)
   }
   __syncthreads();
-  // pass 2: scatter grouped by bin: each key takes the next slot of its bin
-  // (returning atomic on the prefix; afterwards cnt[b] holds the END of bin b)
+  // pass 2: scatter grouped by bin
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const unsigned h = ((br[i] >> 16) & 1u) << 4;
-    const unsigned pos = (atomicAdd(&cnt[br[i] >> 17], 1u << h) >> h) & 0xFFFFu;
+    unsigned pos;
+    if constexpr (RANK) pos = ((cnt[br[i] >> 17] >> h) & 0xFFFFu) + (br[i] & 0xFFFFu);
+    else pos = (atomicAdd(&cnt[br[i] >> 17], 1u << h) >> h) & 0xFFFFu;
     sk[BS::swz((int)pos)] = i * THREADS + tid < size ? k[i] : key_max<W>();
   }
   __syncthreads();
@@ -684,8 +501,10 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, uns
     const int p = warp * 32 * ITEMS;
     if (p < size) {
       const int b = (int)key_shr32(key_sub(sk[BS::swz(p)], lo), shift);
-      // (after pass 2 cnt holds bin ENDS: bin b is [end(b-1), end(b)))
-      const int s = b > 0 ? (int)BS::half(cnt, b - 1) : 0, e = (int)BS::half(cnt, b);
+      // bin b is [start(b), start(b+1)) (RANK: cnt holds starts) or
+      // [end(b-1), end(b)) (cnt holds ends)
+      const int s = RANK ? (int)BS::half(cnt, b) : (b > 0 ? (int)BS::half(cnt, b - 1) : 0);
+      const int e = RANK ? (int)BS::half(cnt, b + 1) : (int)BS::half(cnt, b);
       if (s < p) {
         for (int a = s + 1; a < e; ++a) {
           const W x = sk[BS::swz(a)];

@@ -1467,13 +1467,9 @@ __global__ void __launch_bounds__(SortClass<CLS>::T, final_min_blocks<W, CLS>())
     if constexpr (CLS >= 1) {
       // counting-sort base case; items it rejects (clustered keys, decided
       // block-uniformly) go to the full-width network fallback kernel
-      bool done;
-      if constexpr (sizeof(W) == 8)
-        done = X.flt ? bin_sort_item_rank<W, THREADS, ITEMS, true>(k, size, smem_raw, dst, X)
-                     : bin_sort_item_rank<W, THREADS, ITEMS, false>(k, size, smem_raw, dst, X);
-      else
-        done = X.flt ? bin_sort_item<W, THREADS, ITEMS, true>(k, size, smem_raw, dst, X)
-                     : bin_sort_item<W, THREADS, ITEMS, false>(k, size, smem_raw, dst, X);
+      constexpr bool RANK = sizeof(W) == 8;  // (measured per key width)
+      const bool done = X.flt ? bin_sort_item<W, THREADS, ITEMS, true, RANK>(k, size, dst, X)
+                              : bin_sort_item<W, THREADS, ITEMS, false, RANK>(k, size, dst, X);
       if (!done && threadIdx.x == 0) {
         const unsigned long long slot = atomicAdd(&P.ctrl->item_count[kListFallback], 1ull);
         if (slot < P.cap_items) P.items[kListFallback][slot] = item;

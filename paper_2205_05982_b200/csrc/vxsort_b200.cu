@@ -106,17 +106,67 @@ struct DevInfo {
 std::mutex g_mu;
 std::unordered_map<int, DevInfo> g_dev;
 
-// Keep stream-ordered allocations (workspace, host-path key buffers) cached
-// in the device's default pool instead of returning them at every sync.
+// Stream-ordered allocations (own workspace, host-path key buffers) come
+// from a PRIVATE per-device pool that keeps its memory cached between calls.
+// The device's default pool is left untouched: its attributes belong to the
+// host application (and to torch's allocator next to us).
+std::unordered_map<int, cudaMemPool_t> g_pool;
+
 void ensure_pool(int dev, DevInfo& di) {
   if (di.sms != 0) return;
   cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    unsigned long long thr = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
 }
+
+// (caller holds g_mu)
+cudaMemPool_t pool_for(int dev) {
+  auto it = g_pool.find(dev);
+  if (it != g_pool.end()) return it->second;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.handleTypes = cudaMemHandleTypeNone;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool = nullptr;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+    cudaGetLastError();
+    return g_pool[dev] = nullptr;
+  }
+  unsigned long long thr = ~0ull;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  return g_pool[dev] = pool;
+}
+
+cudaError_t lib_malloc_async(void** p, size_t bytes, cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    pool = pool_for(dev);
+  }
+  if (pool == nullptr) return cudaMallocAsync(p, bytes, st);
+  return cudaMallocFromPoolAsync(p, bytes, pool, st);
+}
+
+// Library-owned stream-ordered buffer: freed on `st` on every exit path.
+struct AsyncBuf {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  AsyncBuf() = default;
+  AsyncBuf(const AsyncBuf&) = delete;
+  AsyncBuf& operator=(const AsyncBuf&) = delete;
+  cudaError_t alloc(size_t bytes, cudaStream_t s) {
+    st = s;
+    return lib_malloc_async(&p, bytes, s);
+  }
+  cudaError_t free() {
+    if (!p) return cudaSuccess;
+    const cudaError_t e = cudaFreeAsync(p, st);
+    p = nullptr;
+    return e;
+  }
+  ~AsyncBuf() { free(); }
+};
 
 int grid_for(const void* fn, int threads, size_t smem) {
   int dev = 0;
@@ -338,17 +388,20 @@ struct SideStreams {
     }
   }
 };
-SideStream* side_stream() {
-  thread_local SideStreams ts;
+// Per (thread, device) cached streams: kSideBaseCase carries the base-case
+// classes under the main one (run_sort); kSideHost the small host-pointer path.
+enum SideKind : int { kSideBaseCase = 0, kSideHost = 1 };
+SideStream* side_stream(int kind = kSideBaseCase) {
+  thread_local SideStreams ts[2];
   int dev = 0;
   cudaGetDevice(&dev);
-  auto it = ts.m.find(dev);
-  if (it != ts.m.end()) return &it->second;
+  auto it = ts[kind].m.find(dev);
+  if (it != ts[kind].m.end()) return &it->second;
   SideStream x;
   if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
   cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
-  return &(ts.m[dev] = x);
+  return &(ts[kind].m[dev] = x);
 }
 
 struct CtrlMirror {
@@ -395,10 +448,10 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
     stats->workspace_bytes = L.total;
   }
   if (n <= 1) return VXS_OK;
-  void* owned = nullptr;
+  AsyncBuf owned;  // released on every exit path (stream-ordered)
   if (ws == nullptr) {
-    VXS_CK(cudaMallocAsync(&owned, L.total, st), "workspace alloc");
-    ws = owned;
+    VXS_CK(owned.alloc(L.total, st), "workspace alloc");
+    ws = owned.p;
   } else if (ws_bytes < L.total) {
     return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: provided workspace is too small");
   }
@@ -430,23 +483,22 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
         if (rs != VXS_OK) return rs;
         ++launches;
       }
-      if (h.error) {  // (final-phase overflow is checked by the error flag below)
-        if (owned) cudaFreeAsync(owned, st);
+      if (h.error)  // (final-phase overflow is checked by the error flag below)
         return fail(VXS_INTERNAL, "vxsort_b200: device scheduler list overflow");
-      }
       if ((h.split_packed[P.cur] >> 40) == 0) break;
       fallback = true;
       batch = 1;
-      if (levels > 64) {
-        if (owned) cudaFreeAsync(owned, st);
-        return fail(VXS_INTERNAL, "vxsort_b200: bucket recursion did not converge");
-      }
+      if (levels > 64) return fail(VXS_INTERNAL, "vxsort_b200: bucket recursion did not converge");
     }
   } else {
     const vxs_status rs = read_ctrl(P.ctrl, h, st);
     if (rs != VXS_OK) return rs;
     ++launches;
   }
+  if (std::getenv("VXSORT_TRACE"))
+    std::fprintf(stderr, "[vxsort n=%zu levels=%d] items c0..c4 %llu %llu %llu %llu %llu copy %llu/%llu\n", n, levels,
+                 h.item_count[0], h.item_count[1], h.item_count[2], h.item_count[3], h.item_count[4],
+                 h.item_count[kListCopySmall], h.item_count[kListCopyBig]);
   ProfScope phase(K_FINAL_PHASE, st);  // (closes at the end of run_sort's final block)
   // The size classes and the equality-bucket copy touch disjoint items: the
   // class holding the most keys runs on the caller's stream, the rest on a
@@ -489,8 +541,14 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
     }
     if (h.item_count[main_cls]) launch_cls(main_cls, st);
     if (ss) {
-      VXS_CK(cudaEventRecord(ss->join, sd), "join");
-      VXS_CK(cudaStreamWaitEvent(st, ss->join, 0), "join wait");
+      // always join (even after a failed record/launch): the workspace is
+      // released on st and must outlive the side-stream kernels
+      const cudaError_t ej = cudaEventRecord(ss->join, sd);
+      const cudaError_t ew = ej == cudaSuccess ? cudaStreamWaitEvent(st, ss->join, 0) : cudaErrorUnknown;
+      if (ej != cudaSuccess || ew != cudaSuccess) {
+        cudaStreamSynchronize(sd);  // last resort: order by the host
+        return cuda_fail(ej != cudaSuccess ? ej : ew, "join");
+      }
     }
   }
   {
@@ -506,7 +564,7 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
     }
   }
   VXS_CK(cudaGetLastError(), "final launch");
-  if (owned) VXS_CK(cudaFreeAsync(owned, st), "workspace free");
+  VXS_CK(owned.free(), "workspace free");
   if (stats) {
     stats->max_depth = (size_t)levels;
     stats->partition_calls = (size_t)h.partition_calls;
@@ -799,9 +857,9 @@ vxs_status host_pipeline(PipeCtx& X, W* h, size_t n, int xf, uint64_t seed, int 
   unsigned char* small = nullptr;
   const size_t bounds_bytes = sizeof(unsigned long long) * C * (S + 1);
   vxs_status st = VXS_OK;
-  cudaError_t e = cudaMallocAsync(&A, n * sizeof(W), X.s_cmp);
-  if (e == cudaSuccess) e = cudaMallocAsync(&B, n * sizeof(W), X.s_cmp);
-  if (e == cudaSuccess) e = cudaMallocAsync(&small, 256 + sizeof(W) * kPipeMaxSlices + bounds_bytes, X.s_cmp);
+  cudaError_t e = lib_malloc_async(reinterpret_cast<void**>(&A), n * sizeof(W), X.s_cmp);
+  if (e == cudaSuccess) e = lib_malloc_async(reinterpret_cast<void**>(&B), n * sizeof(W), X.s_cmp);
+  if (e == cudaSuccess) e = lib_malloc_async(reinterpret_cast<void**>(&small), 256 + sizeof(W) * kPipeMaxSlices + bounds_bytes, X.s_cmp);
   if (e != cudaSuccess) st = cuda_fail(e, "pipeline alloc");
   W* spl = reinterpret_cast<W*>(small);
   unsigned long long* d_bounds = reinterpret_cast<unsigned long long*>(small + 256 + sizeof(W) * kPipeMaxSlices);
@@ -931,7 +989,7 @@ vxs_status host_pipeline(PipeCtx& X, W* h, size_t n, int xf, uint64_t seed, int 
       max_len = std::max(max_len, len);
     }
     max_len = std::max<unsigned long long>(max_len, 1);
-    e = cudaMallocAsync(&Tb, kMergeStreams * max_len * sizeof(W), X.s_cmp);
+    e = lib_malloc_async(reinterpret_cast<void**>(&Tb), kMergeStreams * max_len * sizeof(W), X.s_cmp);
     if (e == cudaSuccess) e = cudaStreamSynchronize(X.s_cmp);
     if (e != cudaSuccess) st = cuda_fail(e, "pipeline merge buffer");
   }
@@ -1107,10 +1165,10 @@ template <typename WK, typename WP, typename V>
 vxs_status run_packed(const WK* keys_in, size_t n, int xf, uint64_t seed, unsigned long long* idx_out, WK* keys_out,
                       V* vals, size_t vb, void* ws, size_t ws_bytes, cudaStream_t st, vxs_stats* stats) {
   const PackLayout L = pack_layout(n, sizeof(WK), vals ? vb : 0);
-  void* owned = nullptr;
+  AsyncBuf owned;
   if (ws == nullptr) {
-    VXS_CK(cudaMallocAsync(&owned, std::max<size_t>(L.total, 256), st), "workspace alloc");
-    ws = owned;
+    VXS_CK(owned.alloc(std::max<size_t>(L.total, 256), st), "workspace alloc");
+    ws = owned.p;
   } else if (ws_bytes < L.total) {
     return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: provided workspace is too small");
   }
@@ -1124,17 +1182,14 @@ vxs_status run_packed(const WK* keys_in, size_t n, int xf, uint64_t seed, unsign
   }
   VXS_CK(cudaGetLastError(), "pack");
   vxs_status s = run_sort<WP>(packed, n, XF_NONE, seed, base + L.sort_ws, L.sort_ws_bytes, st, stats);
-  if (s != VXS_OK) {
-    if (owned) cudaFreeAsync(owned, st);
-    return s;
-  }
+  if (s != VXS_OK) return s;
   {
     ProfScope ps(K_MISC, st);
     k_unpack_index<WK, WP, V><<<g, 256, 0, st>>>(packed, n, xf, idx_out, keys_out, vals, vals ? vtmp : nullptr);
   }
   VXS_CK(cudaGetLastError(), "unpack");
   if (vals) VXS_CK(cudaMemcpyAsync(vals, vtmp, n * vb, cudaMemcpyDeviceToDevice, st), "values copy");
-  if (owned) VXS_CK(cudaFreeAsync(owned, st), "workspace free");
+  VXS_CK(owned.free(), "workspace free");
   if (stats) {
     stats->kernel_launches += 2;
     stats->workspace_bytes = L.total;
@@ -1274,27 +1329,25 @@ vxs_status vxs_sort_host(void* h_keys, size_t n, vxs_key_type type, vxs_order or
       });
     }
   }
-  cudaStream_t st;
-  VXS_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream create");
-  void* d = nullptr;
-  cudaError_t e = cudaMallocAsync(&d, n * kb, st);
-  if (e != cudaSuccess) {
-    cudaStreamDestroy(st);
-    return cuda_fail(e, "key buffer alloc");
-  }
+  // small inputs: copy in, sort, copy out on this thread's cached stream
+  SideStream* hs = side_stream(kSideHost);
+  if (hs == nullptr) return fail(VXS_CUDA_ERROR, "vxsort_b200: stream create failed");
+  cudaStream_t st = hs->s;
   vxs_status s = VXS_OK;
-  e = cudaMemcpyAsync(d, h_keys, n * kb, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) s = cuda_fail(e, "H2D");
-  if (s == VXS_OK) s = vxs_sort(d, n, type, order, seed_for(seed, has_seed, h_keys, n), 1, nullptr, 0, st, stats);
-  if (s == VXS_OK) {
-    e = cudaMemcpyAsync(h_keys, d, n * kb, cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) s = cuda_fail(e, "D2H");
+  {
+    AsyncBuf d;
+    cudaError_t e = d.alloc(n * kb, st);
+    if (e != cudaSuccess) return cuda_fail(e, "key buffer alloc");
+    e = cudaMemcpyAsync(d.p, h_keys, n * kb, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) s = cuda_fail(e, "H2D");
+    if (s == VXS_OK) s = vxs_sort(d.p, n, type, order, seed_for(seed, has_seed, h_keys, n), 1, nullptr, 0, st, stats);
+    if (s == VXS_OK) {
+      e = cudaMemcpyAsync(h_keys, d.p, n * kb, cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) s = cuda_fail(e, "D2H");
+    }
   }
-  cudaFreeAsync(d, st);
-  e = cudaStreamSynchronize(st);
+  const cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess && s == VXS_OK) s = cuda_fail(e, "sync");
-  cudaStreamDestroy(st);
-  if (stats) stats->kernel_launches += 0;
   return s;
 }
 
@@ -1422,11 +1475,11 @@ vxs_status vxs_partition(const void* d_keys, size_t n, vxs_key_type type, vxs_or
       return VXS_OK;
     }
     const Layout Lay = layout_for<W>(n);
-    void* owned = nullptr;
+    AsyncBuf owned;
     void* ws = d_workspace;
     if (ws == nullptr) {
-      VXS_CK(cudaMallocAsync(&owned, Lay.total, st), "workspace alloc");
-      ws = owned;
+      VXS_CK(owned.alloc(Lay.total, st), "workspace alloc");
+      ws = owned.p;
     } else if (workspace_bytes < Lay.total) {
       return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: provided workspace is too small");
     }
@@ -1450,7 +1503,7 @@ vxs_status vxs_partition(const void* d_keys, size_t n, vxs_key_type type, vxs_or
     }
     k_part_counts<W><<<1, 256, 0, st>>>(P, nseg, reinterpret_cast<unsigned long long*>(d_seg_counts));
     VXS_CK(cudaGetLastError(), "partition");
-    if (owned) VXS_CK(cudaFreeAsync(owned, st), "workspace free");
+    VXS_CK(owned.free(), "workspace free");
     return VXS_OK;
   });
 }

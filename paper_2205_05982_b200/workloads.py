@@ -110,7 +110,8 @@ def c5(n, rank=0, skewed=False, seed=1):
 
     def gen(r):
         u = (r >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
-        v = np.ldexp(u ** 4, 64)
+        u2 = u * u
+        v = (u2 * u2) * 2.0 ** 64  # explicit products: bit-identical on the device
         v = np.minimum(v, 2.0 ** 64 - 2.0 ** 11)
         return v.astype(np.uint64)
     return _chunked(s, n, gen, np.uint64)
@@ -135,3 +136,57 @@ def make(name: str, n=None, seed=1, rank=0):
     if name in ("c5", "c5-skew"):
         return c5(n or (1 << 30), rank, name == "c5-skew", seed), "u64", False
     raise ValueError(name)
+
+
+# ---- device-side generation (bench only: 2^30-key configs) -----------------
+# The same counter-based SplitMix64 stream computed with torch int64 ops on
+# the GPU (wrapping multiplies; logical shifts via masks), so an 8 GB C5 input
+# appears in milliseconds instead of a minute of numpy + an 8 GB H2D copy.
+# Bit-identical to splitmix64() above.
+
+def _i64(v: int) -> int:
+    v &= 2**64 - 1
+    return v - 2**64 if v >= 2**63 else v
+
+
+def _shr(z, k: int):
+    import torch
+    return (z >> k) & ((1 << (64 - k)) - 1)
+
+
+def splitmix64_device(seed: int, start: int, n: int, device):
+    import torch
+    z = torch.arange(start + 1, start + n + 1, dtype=torch.int64, device=device)
+    z = z * _i64(0x9E3779B97F4A7C15) + _i64(seed)
+    z = (z ^ _shr(z, 30)) * _i64(0xBF58476D1CE4E5B9)
+    z = (z ^ _shr(z, 27)) * _i64(0x94D049BB133111EB)
+    return z ^ _shr(z, 31)
+
+
+def make_device(name: str, n=None, seed=1, rank=0, device="cuda"):
+    """(device keys, key_type, descending) for the uniform / C5 workloads
+    (same bits as make() for the uniform streams; the skewed stream maps the
+    same uniforms through floor(2^64 * u^4) in float64 on the device)."""
+    import torch
+    if name == "u64-uniform":
+        n = n or 100_000_000
+        return splitmix64_device(seed, 0, n, device).view(torch.uint64), "u64", False
+    if name in ("c5", "c5-skew"):
+        n = n or (1 << 30)
+        s = seed ^ ((rank * 0x9E3779B97F4A7C15) & (2**64 - 1)) ^ 0x6A09E667F3BCC909
+        out = torch.empty(n, dtype=torch.int64, device=device)
+        step = 1 << 26
+        for b in range(0, n, step):
+            e = min(n, b + step)
+            r = splitmix64_device(s, b, e - b, device)
+            if name == "c5-skew":
+                u = _shr(r, 11).to(torch.float64) * (2.0 ** -53)
+                u2 = u * u
+                v = torch.clamp((u2 * u2) * 2.0 ** 64, max=2.0 ** 64 - 2.0 ** 11)
+                # float64 -> uint64 through two int64 halves (v may exceed 2^63)
+                hi = torch.floor(v / 2.0 ** 32)
+                lo = v - hi * 2.0 ** 32
+                r = (hi.to(torch.int64) << 32) | lo.to(torch.int64)
+            out[b:e] = r
+        return out.view(torch.uint64), "u64", False
+    raise ValueError(f"no device generator for {name}")

@@ -61,6 +61,13 @@ def test_invalid_arguments_map_to_value_error():
         vx.sort(np.zeros((4, 2), np.uint64))  # K128 needs an explicit key type
     with pytest.raises(ValueError):
         vx.sort(np.zeros(4, np.complex64))
+    # a 2-D array of a 1-word key type is rejected, not sorted by its first column
+    with pytest.raises(ValueError):
+        vx.sort(np.zeros((4, 3), np.int32), key_type="i32")
+    with pytest.raises(ValueError):
+        vx.sort(np.zeros((4, 3), np.uint64), key_type="k128")
+    with pytest.raises(ValueError):
+        vx.sort(np.zeros((), np.uint32), key_type="u32")
 
 
 def test_trivial_host_sorts_need_no_device():
