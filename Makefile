@@ -1,21 +1,32 @@
 # Builds the product library (sm_100a) and the oracle (test infrastructure).
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -shared -Xcompiler -fPIC -Xcompiler -O3
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3
 PKG := paper_2205_05982_b200
-SRCS := $(wildcard $(PKG)/csrc/*.cu) $(wildcard $(PKG)/csrc/*.cuh) include/vxsort_b200.h
+BUILD := build
+HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/vxsort_b200.h
 
 all: $(PKG)/lib/libvxsort_b200.so oracle
 
-$(PKG)/lib/libvxsort_b200.so: $(SRCS)
+# sort kernels + single-GPU host orchestration (the long compile)
+$(BUILD)/vxsort_b200.o: $(PKG)/csrc/vxsort_b200.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+# distributed sample sort (host orchestration over the C ABI; NCCL via dlopen)
+$(BUILD)/dist_sort.o: $(PKG)/csrc/dist_sort.cu include/vxsort_b200.h
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+$(PKG)/lib/libvxsort_b200.so: $(BUILD)/vxsort_b200.o $(BUILD)/dist_sort.o
 	@mkdir -p $(PKG)/lib
-	$(NVCC) $(NVFLAGS) -o $@ $(PKG)/csrc/vxsort_b200.cu
+	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl
 
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -f $(PKG)/lib/*.so
+	rm -rf $(PKG)/lib/*.so $(BUILD)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean

@@ -390,7 +390,7 @@ def load_workload(name, n=None, rank=0):
     return torch.from_numpy(x).to("cuda"), x, kt, desc
 
 
-def time_extra(wl, peak, steps=3):
+def time_extra(wl, peak, steps=5):
     """One extra workload: validated, timed (device-resident), per-kernel split."""
     import torch
     import paper_2205_05982_b200 as vx
@@ -791,23 +791,24 @@ def run_distributed(args):
                 extra[key] = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
             torch.cuda.empty_cache()
     # e2e through the public API at N GPUs: pinned host keys -> H2D -> dist_sort -> D2H (max over ranks)
+    # one pinned buffer per rank holds the step's input and receives its
+    # result (8 ranks x 8 GB of pinned memory fit the host; two would not)
     stream = torch.cuda.current_stream()
-    host = torch.empty(src.shape, dtype=src.dtype).pin_memory()
-    host.copy_(src)
+    cap = max(n, int(max(allrecv) * 1.1) + 1024)
+    hbuf = torch.empty((cap,) + tuple(src.shape[1:]), dtype=src.dtype).pin_memory()
     dev_in = torch.empty_like(src)
-    cap = int(max(allrecv) * 1.1) + 1024
-    host_out = torch.empty((cap,) + tuple(src.shape[1:]), dtype=src.dtype).pin_memory()
     e2e_times, d2h_bytes = [], 0
     for _ in range(max(1, min(args.steps, 3))):
-        dist.barrier()
+        hbuf[:n].copy_(src)  # restore this step's unsorted input on the host (untimed)
         torch.cuda.synchronize()
+        dist.barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        dev_in.copy_(host, non_blocking=True)
+        dev_in.copy_(hbuf[:n], non_blocking=True)
         res = dist_sort(dev_in, order=order, key_type=kt, exchange=args.exchange, copy_out=False)
-        m = min(res.shape[0], host_out.shape[0])
-        host_out[:m].copy_(res[:m], non_blocking=True)
+        m = min(res.shape[0], cap)
+        hbuf[:m].copy_(res[:m], non_blocking=True)
         b.record(stream)
         torch.cuda.synchronize()
         e2e_times.append(a.elapsed_time(b))
@@ -860,7 +861,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default=None,
                     help=f"default {DEFAULT_SINGLE} on one GPU, {DEFAULT_DIST} (per rank) distributed")
-    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--num-keys", dest="n", type=int, default=None,
+                    help="keys (per rank when distributed); default: the workload's BASELINE size")
     ap.add_argument("--extras", default=DEFAULT_EXTRAS)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: debug mode, ranks may share one GPU (collectives over gloo)")

@@ -196,6 +196,35 @@ SortStats sort_pairs_device(T* d_keys, V* d_values, std::size_t n, const SortCon
   return detail::to_stats(st);
 }
 
+// Distributed sample sort across ranks (one process per GPU),
+// RAII over vxs_dist_create / vxs_dist_destroy.  Every rank of the group
+// constructs, sorts and destroys together.  sort() returns this rank's sorted
+// slice of the union (device memory inside the context's receive window,
+// valid until the next sort()).
+class DistSorter {
+ public:
+  explicit DistSorter(const vxs_dist_group& group) { detail::throw_status(vxs_dist_create(&group, &ctx_)); }
+  DistSorter(const DistSorter&) = delete;
+  DistSorter& operator=(const DistSorter&) = delete;
+  ~DistSorter() { vxs_dist_destroy(ctx_); }
+
+  template <typename T>
+  std::span<T> sort(const T* d_keys, std::size_t n, const SortConfig& config = {}, void* stream = nullptr,
+                    vxs_exchange exchange = VXS_EXCHANGE_FUSED, SortStats* stats = nullptr) {
+    void* out = nullptr;
+    std::size_t n_out = 0;
+    vxs_stats st{};
+    detail::throw_status(vxs_dist_sort(ctx_, d_keys, n, detail::KeyCode<T>::v,
+                                       config.order == Order::kAscending ? VXS_ASCENDING : VXS_DESCENDING,
+                                       config.seed.value_or(1), exchange, &out, &n_out, stream, &st));
+    if (stats) *stats = detail::to_stats(st);
+    return std::span<T>(static_cast<T*>(out), n_out);
+  }
+
+ private:
+  vxs_dist_ctx ctx_ = nullptr;
+};
+
 // The B200 path is data-parallel device code; kept for source compatibility
 // with vexsort.hpp:132.
 inline bool wide_backend_is_simd() { return true; }

@@ -160,6 +160,65 @@ vxs_status vxs_ipc_handle(void* d_ptr, void* handle64);
 vxs_status vxs_ipc_open(const void* handle64, void** d_ptr);
 vxs_status vxs_ipc_close(void* d_ptr);
 
+/* ---- distributed sample sort (SURVEY §8b vxs_dist_sort, §8e) ----------------
+ * Extends the reference's single-array surface (vexsort.hpp:121-129; the
+ * reference itself has no parallel sort) to one rank per GPU:
+ * rank r ends up holding the r-th key range of the union of every rank's
+ * keys, sorted; concatenation in rank order equals the single-array sort.
+ *
+ * vxs_dist_group describes the process group.  With nccl_comm (an
+ * ncclComm_t, e.g. from vxs_nccl_comm_create) the small collectives run on
+ * the device over NCCL; without one, `allgather` (a host callback: every rank
+ * contributes `bytes` from send, recv receives world*bytes in rank order;
+ * returns 0 on success) carries them -- e.g. an MPI/gloo bootstrap, or ranks
+ * sharing one GPU, which NCCL refuses.
+ *
+ * vxs_dist_create keeps per-group state across calls: the symmetric receive
+ * window (one IPC-exported block per rank, mapped by every peer: P2P over
+ * NVLink / NVSwitch), the partition workspace and staging.  Collective: every
+ * rank of the group calls it (and every vxs_dist_sort / vxs_dist_destroy).
+ *
+ * vxs_dist_sort: local sampling (vxs_sample), all-gather of samples, the same
+ * world-1 splitters on every rank, then
+ *   exchange = VXS_EXCHANGE_FUSED: vxs_partition_counts, all-gather of the
+ *     world x world count matrix, vxs_partition_exchange storing each segment
+ *     straight into its owner's window (the all-to-all rides on the scatter's
+ *     stores), a barrier;
+ *   exchange = VXS_EXCHANGE_NCCL: vxs_partition into a local buffer, NCCL
+ *     grouped send/recv (needs nccl_comm);
+ * then a local vxs_sort of the received keys.  *d_out points at this rank's
+ * sorted slice (*n_out keys) inside the context's window: valid until the
+ * next vxs_dist_sort / vxs_dist_destroy on the context.  Synchronises
+ * `stream` (the count matrix sizes the window).  Stats: the local sort's, with
+ * kernel_launches counting every kernel of the call. */
+typedef struct {
+  int rank;
+  int world;
+  void* nccl_comm;
+  int (*allgather)(void* ctx, const void* send, void* recv, size_t bytes);
+  void* allgather_ctx;
+} vxs_dist_group;
+
+typedef enum { VXS_EXCHANGE_FUSED = 0, VXS_EXCHANGE_NCCL = 1 } vxs_exchange;
+
+typedef struct vxs_dist_ctx_s* vxs_dist_ctx;
+
+vxs_status vxs_dist_create(const vxs_dist_group* group, vxs_dist_ctx* out);
+vxs_status vxs_dist_destroy(vxs_dist_ctx ctx);
+vxs_status vxs_dist_sort(vxs_dist_ctx ctx, const void* d_keys, size_t n, vxs_key_type type, vxs_order order,
+                         uint64_t seed, vxs_exchange exchange, void** d_out, size_t* n_out, void* stream,
+                         vxs_stats* stats);
+/* Per-rank key counts of the last vxs_dist_sort (world entries: keys each
+ * rank received) and this rank's per-destination send counts. */
+vxs_status vxs_dist_last_counts(vxs_dist_ctx ctx, uint64_t* recv_per_rank, uint64_t* sent_per_rank);
+
+/* NCCL bootstrap helpers for hosts without their own (NCCL is loaded at run
+ * time; these fail with VXS_CUDA_ERROR when libnccl.so.2 is absent).
+ * vxs_nccl_unique_id writes the 128-byte ncclUniqueId rank 0 must share. */
+vxs_status vxs_nccl_unique_id(void* id128);
+vxs_status vxs_nccl_comm_create(const void* id128, int world, int rank, void** comm);
+vxs_status vxs_nccl_comm_destroy(void* comm);
+
 /* Key transform as used inside the kernels (exposed for tests): encodes
  * (inverse=0) or decodes (inverse=1) n keys in place on the device. */
 vxs_status vxs_transform(void* d_keys, size_t n, vxs_key_type type, vxs_order order, int inverse,

@@ -146,6 +146,17 @@ def lib():
         L.vxs_ipc_handle.argtypes = [vp, vp]
         L.vxs_ipc_open.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p)]
         L.vxs_ipc_close.argtypes = [vp]
+        L.vxs_dist_create.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p)]
+        L.vxs_dist_destroy.argtypes = [vp]
+        L.vxs_dist_sort.argtypes = [vp, vp, sz, i, i, u64, i, ctypes.POINTER(ctypes.c_void_p),
+                                    ctypes.POINTER(ctypes.c_size_t), vp, ctypes.POINTER(SortStats)]
+        L.vxs_dist_last_counts.argtypes = [vp, vp, vp]
+        L.vxs_nccl_unique_id.argtypes = [vp]
+        L.vxs_nccl_comm_create.argtypes = [vp, i, i, ctypes.POINTER(ctypes.c_void_p)]
+        L.vxs_nccl_comm_destroy.argtypes = [vp]
+        for fn in ("vxs_dist_create", "vxs_dist_destroy", "vxs_dist_sort", "vxs_dist_last_counts",
+                   "vxs_nccl_unique_id", "vxs_nccl_comm_create", "vxs_nccl_comm_destroy"):
+            getattr(L, fn).restype = ctypes.c_int
         for fn in ("vxs_sort", "vxs_sort_host", "vxs_sort_workspace_bytes", "vxs_sample",
                    "vxs_partition", "vxs_transform", "vxs_argsort_workspace_bytes", "vxs_argsort",
                    "vxs_sort_pairs", "vxs_partition_counts", "vxs_partition_exchange", "vxs_device_alloc",
@@ -161,7 +172,8 @@ EXPORTED_SYMBOLS = ["vxs_sort_workspace_bytes", "vxs_sort", "vxs_sort_host", "vx
                     "vxs_base_case_capacity", "vxs_version", "vxs_profile_enable",
                     "vxs_profile_reset", "vxs_profile_read", "vxs_partition_counts",
                     "vxs_partition_exchange", "vxs_device_alloc", "vxs_device_free", "vxs_ipc_handle",
-                    "vxs_ipc_open", "vxs_ipc_close"]
+                    "vxs_ipc_open", "vxs_ipc_close", "vxs_dist_create", "vxs_dist_destroy", "vxs_dist_sort",
+                    "vxs_dist_last_counts", "vxs_nccl_unique_id", "vxs_nccl_comm_create", "vxs_nccl_comm_destroy"]
 
 
 class KernelProfile(ctypes.Structure):

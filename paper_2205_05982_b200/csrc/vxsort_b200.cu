@@ -24,9 +24,11 @@
 #include "sample_sort.cuh"
 
 namespace vxs {
-namespace {
 
 thread_local char g_err[512];
+void set_error(const char* msg) { std::snprintf(g_err, sizeof(g_err), "%s", msg); }
+
+namespace {
 
 vxs_status fail(vxs_status s, const char* msg) {
   std::snprintf(g_err, sizeof(g_err), "%s", msg);

@@ -36,13 +36,15 @@ Exchange (step 4) comes in two forms:
 """
 from __future__ import annotations
 
+import ctypes
 from typing import Optional
 
 import torch
 import torch.distributed as dist
 
-from . import (KEY_BYTES, DeviceBlock, Order, SortConfig, infer_key_type, partition, partition_counts,
-               partition_exchange, sample, sort, workspace_bytes)
+from . import (KEY_BYTES, KEY_CODE, DeviceBlock, Order, SortConfig, SortStats, _check, _device_of, _nkeys,
+               _stream_ptr, infer_key_type, lib, partition, partition_counts, partition_exchange, sample, sort,
+               workspace_bytes)
 
 
 class SymmetricWindow:
@@ -245,3 +247,98 @@ def _fused_tail(local, n, kt, kb, spl, order, group, world, rank, ops, timings, 
         timings["recv_keys"] = int(recv)
         timings["send_counts"] = m[rank]
     return out.clone() if copy_out else out
+
+
+# ---- the C-ABI distributed sort (vxs_dist_*, include/vxsort_b200.h) ----------
+_ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t)
+
+
+class _DistGroup(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("world", ctypes.c_int), ("nccl_comm", ctypes.c_void_p),
+                ("allgather", _ALLGATHER_FN), ("allgather_ctx", ctypes.c_void_p)]
+
+
+class NativeDist:
+    """Python handle on the C++ distributed sort (``vxs_dist_sort``): the
+    whole sample sort -- sampling, splitters, exchange, local sort -- runs in
+    the library; Python only supplies the process group.
+
+    ``comm="nccl"``: a native NCCL communicator (bootstrapped over the torch
+    group), the small collectives on the device.  ``comm="host"``: the
+    library's host all-gather callback over a CPU (gloo) group -- works when
+    ranks share a GPU, which NCCL refuses.  Collective: every rank of the
+    group constructs, sorts and closes together."""
+
+    def __init__(self, group=None, comm: str = "host"):
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.comm = None
+        self._cpu_group = None
+        self._cb = _ALLGATHER_FN(0)
+        if comm == "nccl":
+            idb = ctypes.create_string_buffer(128)
+            if self.rank == 0:
+                _check(lib().vxs_nccl_unique_id(idb))
+            obj = [idb.raw]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            idb = ctypes.create_string_buffer(obj[0], 128)
+            out = ctypes.c_void_p()
+            _check(lib().vxs_nccl_comm_create(idb, self.world, self.rank, ctypes.byref(out)))
+            self.comm = out.value
+        elif self.world > 1:
+            backend = dist.get_backend(group)
+            self._cpu_group = group if backend == "gloo" else dist.new_group(backend="gloo")
+            self._cb = _ALLGATHER_FN(self._allgather)
+        g = _DistGroup(self.rank, self.world, self.comm, self._cb, None)
+        out = ctypes.c_void_p()
+        _check(lib().vxs_dist_create(ctypes.byref(g), ctypes.byref(out)))
+        self.ctx = out.value
+
+    def _allgather(self, _ctx, send, recv, nbytes):
+        try:
+            src = torch.frombuffer(bytearray(ctypes.string_at(send, nbytes)), dtype=torch.uint8)
+            dst = torch.empty(self.world * nbytes, dtype=torch.uint8)
+            dist.all_gather_into_tensor(dst, src, group=self._cpu_group)
+            ctypes.memmove(recv, dst.data_ptr(), self.world * nbytes)
+            return 0
+        except Exception:  # noqa: BLE001  (reported to the library as a failed collective)
+            return 1
+
+    def sort(self, keys: torch.Tensor, order: Order = Order.kAscending, key_type: Optional[str] = None,
+             seed: int = 1, exchange: str = "fused", stream=None):
+        """This rank's sorted slice of the union of every rank's ``keys`` --
+        a view of the context's receive window, valid until the next sort or
+        close.  Returns (tensor, SortStats)."""
+        kt = infer_key_type(keys, key_type)
+        if not keys.is_cuda or not keys.is_contiguous():
+            raise ValueError("keys must be a contiguous CUDA tensor")
+        n = _nkeys(keys, kt)
+        d_out = ctypes.c_void_p()
+        n_out = ctypes.c_size_t()
+        st = SortStats()
+        with _device_of(keys):
+            _check(lib().vxs_dist_sort(self.ctx, keys.data_ptr() if n else None, n, KEY_CODE[kt], int(order),
+                                       int(seed) & (2**64 - 1), 0 if exchange == "fused" else 1,
+                                       ctypes.byref(d_out), ctypes.byref(n_out), _stream_ptr(stream),
+                                       ctypes.byref(st)))
+        kb = KEY_BYTES[kt]
+        m = int(n_out.value)
+        blk = DeviceBlock(max(m * kb, 1), ptr=d_out.value, owned=False)
+        raw = torch.as_tensor(blk, device=keys.device)[: m * kb]
+        shape = (m, 2) if kb == 16 else (m,)
+        return raw.view(keys.dtype).reshape(shape), st
+
+    def last_counts(self):
+        """(keys received per rank, this rank's keys sent per destination)."""
+        r = (ctypes.c_uint64 * self.world)()
+        s_ = (ctypes.c_uint64 * self.world)()
+        _check(lib().vxs_dist_last_counts(self.ctx, r, s_))
+        return list(r), list(s_)
+
+    def close(self):
+        if self.ctx:
+            _check(lib().vxs_dist_destroy(self.ctx))
+            self.ctx = None
+        if self.comm:
+            _check(lib().vxs_nccl_comm_destroy(self.comm))
+            self.comm = None

@@ -70,6 +70,21 @@ def test_invalid_arguments_map_to_value_error():
         vx.sort(np.zeros((), np.uint32), key_type="u32")
 
 
+def test_dist_create_validates_the_group():
+    """vxs_dist_create rejects bad groups before touching a device."""
+    from paper_2205_05982_b200.dist import _ALLGATHER_FN, _DistGroup
+    lib = vx.lib()
+    out = ctypes.c_void_p()
+    for rank, world in ((0, 0), (2, 2), (-1, 1)):
+        g = _DistGroup(rank, world, None, _ALLGATHER_FN(0), None)
+        assert lib.vxs_dist_create(ctypes.byref(g), ctypes.byref(out)) == 1
+    g = _DistGroup(0, 2, None, _ALLGATHER_FN(0), None)  # world > 1 needs NCCL or a host all-gather
+    assert lib.vxs_dist_create(ctypes.byref(g), ctypes.byref(out)) == 1
+    assert b"allgather" in lib.vxs_last_error()
+    assert lib.vxs_dist_sort(None, None, 0, 6, 0, 1, 0, ctypes.byref(out), ctypes.byref(ctypes.c_size_t()),
+                             None, None) == 1
+
+
 def test_trivial_host_sorts_need_no_device():
     # n <= 1 returns before touching the device (driver.hpp:175)
     for n in (0, 1):
