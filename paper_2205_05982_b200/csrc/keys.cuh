@@ -214,17 +214,17 @@ __host__ __device__ __forceinline__ W flt_enc(W b, bool desc) {
   const W expm = ((W(1) << (B - 1 - M)) - 1) << M;  // exponent mask
   const W mant = (W(1) << M) - 1;                    // NaN payloads per sign
   const W nn = W(0) - W(2) * mant;                   // # non-NaN values (mod 2^B)
-  const bool is_nan = ((b & expm) == expm) && (b & mant) != 0;
-  if (is_nan) {
-    // Positive NaNs (raw bits ascending) then negative NaNs, after all
-    // non-NaN keys, in both orders.
-    const bool neg = (b & sign) != 0;
-    const W base = neg ? (expm | sign) + 1 : expm + 1;
-    return nn + (neg ? mant : W(0)) + (b - base);
-  }
-  const W to = (b & sign) ? W(~b) : W(b ^ sign);  // IEEE totalOrder key
-  const W t = to - mant;                          // shift out the negative NaNs
-  return desc ? W(nn - W(1) - t) : t;
+  // IEEE totalOrder key, shifted down by the negative-NaN slots: non-NaN keys
+  // land on [0, nn), positive NaNs (raw bits ascending) on [nn, nn + mant);
+  // negative NaNs keep their raw bits, which are exactly [nn + mant, 2^B) in
+  // raw order.  So NaNs follow every non-NaN key, ordered by raw bits, and
+  // only the non-NaN keys are reversed for descending order.  Branch-free:
+  // a handful of ALU ops per key on the first read of a level.
+  const W to = (b & sign) ? W(~b) : W(b ^ sign);
+  const W t = b > (expm | sign) ? b : W(to - mant);
+  if (!desc) return t;
+  const bool is_nan = W(b & ~sign) > expm;
+  return is_nan ? t : W(nn - W(1) - t);
 }
 
 template <typename W>
@@ -235,12 +235,9 @@ __host__ __device__ __forceinline__ W flt_dec(W t, bool desc) {
   const W expm = ((W(1) << (B - 1 - M)) - 1) << M;
   const W mant = (W(1) << M) - 1;
   const W nn = W(0) - W(2) * mant;
-  if (t >= nn) {
-    const W idx = t - nn;
-    return idx < mant ? W(expm + 1 + idx) : W((expm | sign) + 1 + (idx - mant));
-  }
-  const W u = desc ? W(nn - W(1) - t) : t;
-  const W to = u + mant;
+  if (desc && t < nn) t = W(nn - W(1) - t);  // (NaN words are not reversed)
+  if (t > (expm | sign)) return t;           // negative NaNs: raw bits
+  const W to = t + mant;                     // positive NaNs decode like the rest
   return (to & sign) ? W(to ^ sign) : W(~to);
 }
 

@@ -51,8 +51,9 @@ enum : unsigned { F_IN_B = 1u, F_RAW = 2u };
 struct SplitDesc {
   unsigned long long start, size, tile_base;
   unsigned long long aux;  // radix mode: digit multiplier M (digit = f * M >> 32)
-  unsigned flags, L;       // L: bits 0-7 fan-out exponent, bit 8 radix mode, bits 16-23 shift,
-                           //    bits 24-31 distinct splitter count when < 2^L - 1
+  unsigned flags, L;       // L: bits 0-7 fan-out exponent, bit 8 radix mode, bit 9 piecewise
+                           //    radix over the splitters, bits 16-23 shift, bits 24-31 distinct
+                           //    splitter count when < 2^L - 1
 };
 
 struct Item {
@@ -66,6 +67,7 @@ struct Ctrl {
   unsigned long long item_count[kNumLists];
   unsigned long long partition_calls, keys_partitioned, base_cases;
   unsigned error, pad;
+  unsigned modes[8][4];  // (diagnostics) buckets per level: splitter table/tree, radix, piecewise radix
 };
 
 // Compile-time configuration per key word: the classify/scatter tile (keys
@@ -265,15 +267,22 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* total, T* scratch /*[3
   return r;
 }
 
-// Splitters of one bucket in shared memory, with a lookup table that guides
-// classification: the key range [lo, hi] of the splitters is cut into 2^11
-// equal cells and lut[c] = #splitters < (first key of cell c).  A key's
-// child index (its lower bound among the splitters) lies in [lut[c],
-// lut[c+1]], so typical keys need one table load and 0-1 splitter
-// comparisons instead of an 8-level tree walk (binary search inside the
-// cell keeps skewed splitter sets exact and O(log)).
+// Splitters of one bucket in shared memory, with a two-level lookup table
+// that guides classification.  The splitter range [lo, hi] is cut into 2^21
+// fine units of 2^shift codes; the top 9 bits of a key's fine unit pick a
+// first-level bucket, and each bucket owns 2^k consecutive table cells (k
+// from the number of splitters in it: 0 for <= 1, else ~4-8 cells per
+// splitter), so clustered splitter sets (normal floats, skewed keys) get
+// their resolution where the splitters are.  lut[c] = (#splitters < first key
+// of cell c, same for cell c+1): a key's child index (its lower bound among
+// the splitters) lies in that range, so typical keys need two table loads and
+// 0-1 splitter comparisons instead of an 8-level tree walk (binary search
+// inside the rare wider cell keeps any splitter set exact).
 constexpr int kLutBits = 12;
-constexpr int kLut = 1 << kLutBits;
+constexpr int kLut = 1 << kLutBits;  // table cells
+constexpr int kL1Bits = 9;           // first-level buckets
+constexpr int kL1 = 1 << kL1Bits;
+constexpr int kSubBits = 12;         // fine-unit bits below a first-level bucket
 
 // Radix-mode digit of x: f = (max(x, lo) - lo) >> shift (top ~24 varying
 // bits of the bucket's sample range, saturated to 32 bits for keys far above
@@ -306,15 +315,53 @@ __device__ __forceinline__ unsigned radix_digit(const U128& x, const U128& lo, i
 
 template <typename W>
 struct SplSmem {
-  W srt[257];   // m splitters, padded with the maximum up to 255, + sentinel
-  W tree[256];  // implicit BST over srt[0..254] in BFS order (tree[1..255])
+  W srt[257];  // m splitters, padded with the maximum up to 255, + sentinel
+  union {
+    W tree[256];      // implicit BST over srt[0..254] in BFS order (tree[1..255]), tree mode
+    unsigned t1[kL1];  // first-level table: cell base | k << 16, table mode
+  };
   W lo;
-  unsigned cmax;
+  unsigned cmax;  // table modes: raw unit of the last splitter (keys above clamp to it)
+  int lshift;     // table modes: fine unit = min(raw unit, cmax) << lshift (small ranges)
+  int tdepth;     // tree mode: levels (2^tdepth - 1 >= m; shallow for few splitters)
   int shift, m, use_tree;  // use_tree: 0 table, 1 tree, 2 radix (equal-width digits),
                            //   3 radix on the high word (64-bit keys, shift >= 32)
   unsigned mul;  // radix mode multiplier (radix_digit)
   unsigned short lut[kLut];  // (first, end) splitter index of cell c, packed lo | hi << 8
 };
+
+// Table cell of key x (table mode).
+// Fine unit (< 2^21) of key x over the splitter range [lo, hi]: raw unit
+// (x - lo) >> rsh, clamped to the last splitter's, then << lsh so small ranges
+// also spread over all 2^21 units.  Monotone in x.
+template <typename W>
+__device__ __forceinline__ unsigned fine_unit(const W& x, const W& lo, int rsh, int lsh, unsigned cmax) {
+  unsigned cf = key_shr32(key_sub(x, lo), rsh);
+  cf = cf < cmax ? cf : cmax;
+  cf = key_lt(x, lo) ? 0u : cf;
+  return cf << lsh;
+}
+// First key of fine unit u (false if beyond hi).
+template <typename W>
+__device__ __forceinline__ bool unit_start(const W& lo, const W& hi, unsigned u, int rsh, int lsh, W& out) {
+  if (lsh) return cell_start<W>(lo, hi, (u + (1u << lsh) - 1) >> lsh, 0, out);
+  return cell_start<W>(lo, hi, u, rsh, out);
+}
+// Geometry of a splitter range: rsh / lsh / cmax for fine_unit.
+template <typename W>
+__device__ __forceinline__ void fine_geometry(const W& range, int& rsh, int& lsh, unsigned& cmax) {
+  const int bl = key_bitlen(range);
+  rsh = bl > kL1Bits + kSubBits ? bl - (kL1Bits + kSubBits) : 0;
+  lsh = bl < kL1Bits + kSubBits ? kL1Bits + kSubBits - bl : 0;
+  cmax = key_shr32(range, rsh);
+}
+
+template <typename W>
+__device__ __forceinline__ unsigned lut_cell(const W& x, const SplSmem<W>& S) {
+  const unsigned cf = fine_unit(x, S.lo, S.shift, S.lshift, S.cmax);
+  const unsigned t = S.t1[cf >> kSubBits];
+  return (t & 0xFFFFu) + ((cf & ((1u << kSubBits) - 1)) >> (kSubBits - (t >> 16)));
+}
 
 template <typename W>
 __device__ __forceinline__ int lower_bound_smem(const W* srt, int lo, int hi, const W& x) {
@@ -324,6 +371,71 @@ __device__ __forceinline__ int lower_bound_smem(const W* srt, int lo, int hi, co
     else hi = mid;
   }
   return lo;
+}
+
+// Piecewise-radix digit (use_tree 4): first-level bucket c1 of x holds n
+// splitters, t1[c1] = (#splitters before the bucket) | n << 16, and the
+// bucket is cut into n equal-width digits.  Digits ascend with the keys (an
+// empty bucket's keys join the next bucket's first digit); every digit spans
+// about one quantile of the sample when the density is smooth inside a
+// bucket (normal floats: a bucket is at most one exponent band), so children
+// stay balanced with one near-broadcast table load per key and no splitter
+// compare.  Digits lie in [0, m).
+template <typename W>
+__device__ __forceinline__ unsigned pw_digit(const W& x, const W& lo, int rsh, int lsh, unsigned cmax,
+                                             const unsigned* t1) {
+  const unsigned cf = fine_unit(x, lo, rsh, lsh, cmax);
+  const unsigned t = t1[cf >> kSubBits];
+  return (t & 0xFFFFu) + (((cf & ((1u << kSubBits) - 1)) * (t >> 16)) >> kSubBits);
+}
+
+// First-level table over m sorted splitters srt[]: t1[j] = #splitters below
+// bucket j | #splitters inside it << 16.  Thread 0 has set lo / shift / cmax
+// (and a barrier followed).  Returns the bucket count.
+template <typename W>
+__device__ __forceinline__ int build_t1(const W* srt, int m, const W& lo, const W& hi, int rsh, int lsh,
+                                        unsigned cmax, unsigned* t1) {
+  const int n1 = (int)((cmax << lsh) >> kSubBits) + 1;
+  for (int j = threadIdx.x; j < n1; j += blockDim.x) {
+    W s0, s1;
+    const unsigned f0 =
+        unit_start<W>(lo, hi, (unsigned)j << kSubBits, rsh, lsh, s0) ? lower_bound_smem(srt, 0, m, s0) : m;
+    const unsigned f1 = (j + 1 < n1 && unit_start<W>(lo, hi, (unsigned)(j + 1) << kSubBits, rsh, lsh, s1))
+                            ? lower_bound_smem(srt, 0, m, s1)
+                            : (unsigned)m;
+    t1[j] = f0 | ((f1 - f0) << 16);
+  }
+  __syncthreads();
+  return n1;
+}
+
+// Exclusive scan in place over v[0..count), count <= kL1, by the whole CTA
+// (two values per thread at most); returns the total to every thread.
+__device__ __forceinline__ unsigned block_scan_small(unsigned* v, int count, unsigned* warp_tot /*[32]*/) {
+  const int per = (count + (int)blockDim.x - 1) / (int)blockDim.x;  // 1 or 2
+  const int j0 = threadIdx.x * per;
+  unsigned a = j0 < count ? v[j0] : 0u;
+  unsigned b = (per > 1 && j0 + 1 < count) ? v[j0 + 1] : 0u;
+  const unsigned mine = a + b;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  unsigned before = 0, total = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    before += w < warp ? warp_tot[w] : 0u;
+    total += warp_tot[w];
+  }
+  const unsigned ex = before + incl - mine;
+  if (j0 < count) v[j0] = ex;
+  if (per > 1 && j0 + 1 < count) v[j0 + 1] = ex + a;
+  __syncthreads();
+  return total;
 }
 
 // Shared-histogram slot of child c: even children (key ranges; the only
@@ -336,15 +448,26 @@ __host__ __device__ __forceinline__ int hslot(int c) { return (c >> 1) | ((c & 1
 // equality bucket of the maximum key, used when the tree pads with it).
 __host__ __device__ __forceinline__ int num_children(int L) { return 2 * ((1 << L) - 1) + 2; }
 
-// Load a bucket's splitters, build the lookup table and the tree, and pick
-// the classifier: the table when no cell holds more than 2 splitters for
-// more than a few splitters (uniform-ish key codes), else the 8-level tree
-// (clustered codes, e.g. normal floats or few distinct values).
+// Implicit BST of depth D over srt[0 .. 2^D - 1) (BFS order, tree[1 ..
+// 2^D)); the padding with the maximum key keeps lower-bound semantics.
+template <typename W>
+__device__ __forceinline__ void build_tree(SplSmem<W>& S, int D) {
+  for (int j = threadIdx.x + 1; j < (1 << D); j += blockDim.x) {
+    const int d = 31 - __clz(j);
+    const int q = j - (1 << d);
+    S.tree[j] = S.srt[((2 * q + 1) << (D - 1 - d)) - 1];
+  }
+  if (threadIdx.x == 0) S.tdepth = D;
+}
+
+// Load a bucket's splitters, build the two-level lookup table, and pick the
+// classifier: the table when no cell holds more than 2 splitters for more
+// than a few splitters, else the 8-level tree (extremely clustered codes).
 template <typename W>
 __device__ __forceinline__ void load_splitters(const W* g_srt, unsigned lraw, SplSmem<W>& S,
                                                unsigned long long aux = 0) {
-  __shared__ unsigned char first[kLut + 1];
   __shared__ int s_wide;
+  __shared__ unsigned s_tot[32];
   const int L = (int)(lraw & 0xFFu);
   const int m = (lraw >> 24) ? (int)(lraw >> 24) : (1 << L) - 1;  // deduplicated count, if set
   if (lraw & 0x100u) {  // radix mode: digit = (x - lo) >> shift, no table
@@ -352,6 +475,7 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, unsigned lraw, Sp
     if (threadIdx.x == 0) {
       S.lo = g_srt[0];
       S.shift = (int)((lraw >> 16) & 0xFFu);
+      S.lshift = 0;
       S.m = m;
       S.mul = (unsigned)aux;
       S.use_tree = (sizeof(W) == 8 && S.shift >= 32) ? 3 : 2;
@@ -368,35 +492,68 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, unsigned lraw, Sp
   __syncthreads();
   if (threadIdx.x == 0) {
     S.lo = S.srt[0];
-    const W range = key_sub(S.srt[m - 1], S.lo);
-    const int bl = key_bitlen(range);
-    S.shift = bl > kLutBits ? bl - kLutBits : 0;
-    S.cmax = key_shr32(range, S.shift);
+    fine_geometry(key_sub(S.srt[m - 1], S.lo), S.shift, S.lshift, S.cmax);
     S.m = m;
   }
-  for (int j = threadIdx.x + 1; j < 256; j += blockDim.x) {
-    const int d = 31 - __clz(j);
-    const int q = j - (1 << d);
-    S.tree[j] = S.srt[((2 * q + 1) << (7 - d)) - 1];
+  __syncthreads();
+  if (m <= 15) {  // few splitters (low-entropy keys): a shallow tree, <= 4 near-broadcast loads
+    build_tree(S, 32 - __clz((unsigned)m));
+    if (threadIdx.x == 0) S.use_tree = 1;
+    __syncthreads();
+    return;
+  }
+  const W lo = S.lo, hi = S.srt[m - 1];
+  const int sh = S.shift, lsh = S.lshift;
+  const int n1 = build_t1(S.srt, m, lo, hi, sh, lsh, S.cmax, S.t1);
+  if (lraw & 0x200u) {  // piecewise radix (certified by k_sample): t1 is the whole classifier
+    if (threadIdx.x == 0) S.use_tree = 4;
+    __syncthreads();
+    return;
+  }
+  // two-level table: splitters per bucket -> k (cells 2^k) -> cell bases
+  for (int j = threadIdx.x; j < n1; j += blockDim.x) {
+    const unsigned c = S.t1[j] >> 16;  // splitters inside bucket j
+    const unsigned k = c <= 1 ? 0u : umin(32u - __clz(c - 1) + 2u, (unsigned)kSubBits);
+    S.t1[j] = 1u << k;  // (cells; at most 8 per splitter + 1 per bucket: <= 2552 in all)
+    S.lut[j] = (unsigned short)k;  // (k parked in the table until the cells are built)
   }
   __syncthreads();
-  const W lo = S.lo, hi = S.srt[m - 1];
-  const int sh = S.shift;
-  for (int c = threadIdx.x; c <= kLut; c += blockDim.x) {
+  const unsigned ncell = block_scan_small(S.t1, n1, s_tot);
+  for (int j = threadIdx.x; j < n1; j += blockDim.x) S.t1[j] |= (unsigned)S.lut[j] << 16;
+  __syncthreads();
+  // cells: first splitter index of each cell (low byte), then pack (first, end)
+  for (int c = threadIdx.x; c < (int)ncell; c += blockDim.x) {
+    int a = 0, b = n1 - 1;  // bucket owning cell c: the last j with base(j) <= c
+    while (a < b) {
+      const int mid = (a + b + 1) >> 1;
+      if ((S.t1[mid] & 0xFFFFu) <= (unsigned)c) a = mid;
+      else b = mid - 1;
+    }
+    const unsigned t = S.t1[a];
+    const unsigned u = ((unsigned)a << kSubBits) + (((unsigned)c - (t & 0xFFFFu)) << (kSubBits - (t >> 16)));
     W cs;
-    first[c] = cell_start<W>(lo, hi, (unsigned)c, sh, cs) ? (unsigned char)lower_bound_smem(S.srt, 0, m, cs)
-                                                          : (unsigned char)m;
+    S.lut[c] = (unsigned short)(unit_start<W>(lo, hi, u, sh, lsh, cs) ? lower_bound_smem(S.srt, 0, m, cs) : m);
   }
+  if (threadIdx.x == 0) S.lut[ncell] = (unsigned short)m;  // (ncell <= 2552 < kLut: sentinel slot)
   __syncthreads();
   int wide = 0;
-  for (int c = threadIdx.x; c < kLut; c += blockDim.x) {
-    S.lut[c] = (unsigned short)(first[c] | ((unsigned)first[c + 1] << 8));
-    const int occ = (int)first[c + 1] - (int)first[c];
-    if (occ > 1) wide += occ;
+  for (int c0 = 0; c0 < (int)ncell; c0 += blockDim.x) {  // (block-uniform trip count)
+    const int c = c0 + threadIdx.x;
+    const unsigned e = c < (int)ncell ? S.lut[c + 1] & 0xFFu : 0u;
+    __syncthreads();
+    if (c < (int)ncell) {
+      const unsigned f = S.lut[c] & 0xFFu;
+      S.lut[c] = (unsigned short)(f | (e << 8));
+      const int occ = (int)e - (int)f;
+      if (occ > 2) wide += occ;
+    }
+    __syncthreads();
   }
   if (wide) atomicAdd(&s_wide, wide);
   __syncthreads();
-  if (threadIdx.x == 0) S.use_tree = s_wide > 8 ? 1 : 0;
+  const bool tree = s_wide > 8;  // (block-uniform)
+  if (tree) build_tree(S, 8);    // the table is too coarse: full tree instead (overwrites t1)
+  if (threadIdx.x == 0) S.use_tree = tree ? 1 : 0;
   __syncthreads();
 }
 
@@ -405,42 +562,50 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, unsigned lraw, Sp
 // order: normal_0 < eq_0 < normal_1 < ... < normal_m.
 //
 // Table path: keys below the first splitter use cell 0, keys above the last
-// use the last cell; the answer always lies in [first(c), end(c)] and
-// srt[end(c)] >= x (sentinel), so two unguarded steps finish any cell holding
-// <= 2 splitters; wider cells return -1 for classify_slow.
+// use the last cell; the answer always lies in [first(c), end(c)], so one or
+// two splitter compares finish any cell holding <= 2 splitters; wider cells
+// return -1 for classify_slow.
 // Tree path: branch-free 8-level walk over the padded implicit BST (padding
 // with the maximum key keeps lower-bound semantics; the maximum key itself
 // lands in equality bucket 2m+1).
 template <int MODE, typename W>
 __device__ __forceinline__ int classify_mode(const W& x, const SplSmem<W>& S) {
-  if constexpr (MODE == 3 && sizeof(W) == 8) {
+  if constexpr (MODE == 4) {
+    return 2 * (int)pw_digit(x, S.lo, S.shift, S.lshift, S.cmax, S.t1);
+  } else if constexpr (MODE == 3 && sizeof(W) == 8) {
     return 2 * (int)radix_digit_hi(x, S.lo, S.shift, S.mul, (unsigned)S.m);
   } else if constexpr (MODE >= 2) {
     // equal-width digits over the sample range (the sample certified them
     // balanced); keys below/above the range clamp to the first/last digit
     return 2 * (int)radix_digit(x, S.lo, S.shift, S.mul, (unsigned)S.m);
   } else if constexpr (MODE == 1) {
+    const int D = S.tdepth;  // (block-uniform)
     int j = 1;
 #pragma unroll
-    for (int l = 0; l < 8; ++l) j = 2 * j + (key_lt(S.tree[j], x) ? 1 : 0);
-    const int i = j - 256;
-    const int eq = (i < 255 && key_eq(S.srt[i], x)) ? 1 : 0;
+    for (int l = 0; l < 8; ++l)
+      if (l < D) j = 2 * j + (key_lt(S.tree[j], x) ? 1 : 0);
+    const int i = j - (1 << D);
+    const int eq = (i < (1 << D) - 1 && key_eq(S.srt[i], x)) ? 1 : 0;
     return 2 * i + eq;
   } else {
     // Cell c holds splitters [i, e).  e == i: answer i, no equality possible
     // (srt[i] >= end of cell > x).  e == i+1: one compare with srt[i] gives
     // the answer and the equality bit.  Wider cells take the slow path.
-    unsigned c = key_shr32(key_sub(x, S.lo), S.shift);
-    c = c < S.cmax ? c : S.cmax;
-    c = key_lt(x, S.lo) ? 0u : c;
-    const unsigned pr = S.lut[c];
+    const unsigned pr = S.lut[lut_cell(x, S)];
     const int i = (int)(pr & 0xFFu);
     const int e = (int)(pr >> 8);
     const W sp = S.srt[i];
     const bool has = e > i;
     const bool lt = has && key_lt(sp, x);
-    const bool eq = has && !lt && key_eq(sp, x);
-    return e - i > 1 ? -1 : 2 * (i + (lt ? 1 : 0)) + (eq ? 1 : 0);
+    bool eq = has && !lt && key_eq(sp, x);
+    int r = i + (lt ? 1 : 0);
+    if (e - i == 2 && lt) {  // two splitters in the cell (e.g. -0.0 / +0.0, adjacent codes): one more compare
+      const W sp1 = S.srt[i + 1];
+      const bool lt1 = key_lt(sp1, x);
+      r += lt1 ? 1 : 0;
+      eq = !lt1 && key_eq(sp1, x);
+    }
+    return e - i > 2 ? -1 : 2 * r + (eq ? 1 : 0);
   }
 }
 
@@ -452,8 +617,15 @@ struct RadixReg {
   int shift;
   unsigned m;
   unsigned mul;
-  __device__ __forceinline__ explicit RadixReg(const SplSmem<W>& S) : lo(S.lo), shift(S.shift), m((unsigned)S.m), mul(S.mul) {}
+  unsigned cmax;
+  int lshift;
+  const unsigned* t1;
+  bool pw;  // piecewise radix (mode 4; block-uniform)
+  __device__ __forceinline__ explicit RadixReg(const SplSmem<W>& S)
+      : lo(S.lo), shift(S.shift), m((unsigned)S.m), mul(S.mul), cmax(S.cmax), lshift(S.lshift), t1(S.t1),
+        pw(S.use_tree == 4) {}
   __device__ __forceinline__ int child(const W& x) const {
+    if (pw) return 2 * (int)pw_digit(x, lo, shift, lshift, cmax, t1);
     if constexpr (sizeof(W) == 8) return 2 * (int)radix_digit_hi(x, lo, shift, mul, m);  // (mode 3 only)
     else return 2 * (int)radix_digit(x, lo, shift, mul, m);
   }
@@ -461,17 +633,15 @@ struct RadixReg {
 
 template <typename W>
 __device__ __forceinline__ int classify_fast(const W& x, const SplSmem<W>& S) {
-  return S.use_tree == 3 ? classify_mode<3>(x, S)
+  return S.use_tree == 4 ? classify_mode<4>(x, S)
+         : S.use_tree == 3 ? classify_mode<3>(x, S)
                         : S.use_tree == 2 ? classify_mode<2>(x, S)
                                           : (S.use_tree ? classify_mode<1>(x, S) : classify_mode<0>(x, S));
 }
 
 template <typename W>
 __device__ __noinline__ int classify_slow(const W& x, const SplSmem<W>& S) {
-  unsigned c = key_shr32(key_sub(x, S.lo), S.shift);
-  c = c < S.cmax ? c : S.cmax;
-  c = key_lt(x, S.lo) ? 0u : c;
-  const unsigned pr = S.lut[c];
+  const unsigned pr = S.lut[lut_cell(x, S)];
   const int i = lower_bound_smem(S.srt, (int)(pr & 0xFFu), (int)(pr >> 8), x);
   const int eq = (i < S.m && key_eq(S.srt[i], x)) ? 1 : 0;
   return 2 * i + eq;
@@ -507,6 +677,7 @@ __global__ void k_init(Params<W> P) {
   for (int i = 0; i < kNumLists; ++i) c->item_count[i] = 0;
   c->partition_calls = c->keys_partitioned = c->base_cases = 0;
   c->error = 0;
+  for (int i = 0; i < 32; ++i) c->modes[i / 4][i % 4] = 0;
   if (P.n > (unsigned long long)Cfg<W>::kCap || P.part_mode) {
     SplitDesc d;
     d.start = 0;
@@ -539,6 +710,11 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
   W* s = reinterpret_cast<W*>(smem_raw);
   __shared__ unsigned dcnt[1 << kMaxRadixL];
   __shared__ unsigned s_maxc;
+  __shared__ W s_spl[256];     // deduplicated splitters (piecewise certification)
+  __shared__ unsigned s_t1[kL1];
+  __shared__ W s_pwlo;
+  __shared__ int s_pwsh, s_pwlsh;
+  __shared__ unsigned s_pwcmax;
   __shared__ W s_red_lo[THREADS / 32];
   __shared__ W s_red_hi[THREADS / 32];
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
@@ -638,6 +814,7 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
       while ((1 << Lf) < Dr) ++Lf;
     }
     unsigned meff = 0;  // distinct splitters when fewer than m (bits 24-31 of L)
+    bool pw = false;    // piecewise radix over the splitters (bit 9 of L)
     if (radix) {
       if (threadIdx.x == 0) g[0] = slo;
     } else {
@@ -670,16 +847,45 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
       }
       unsigned u = 0;
       const unsigned pos = block_exclusive_scan<THREADS>(uq, &u, reinterpret_cast<unsigned*>(dcnt));
-      if (uq) g[pos] = v;
+      if (uq) {
+        g[pos] = v;
+        s_spl[pos] = v;
+      }
       if (u < (unsigned)m) {
         Lf = 1;
         while ((1u << Lf) - 1u < u) ++Lf;
         meff = u;
       }
+      // Piecewise-radix certification (pw_digit): equal-width digits inside
+      // each first-level bucket, as many as the bucket holds splitters; taken
+      // when no digit gets more than ~2x its share of the sample (smooth
+      // densities, e.g. normal floats), so keys skip the table + splitter
+      // search.  Low-entropy samples (duplicates) fail it and keep the
+      // splitters' equality buckets.
+      const int mq = (int)u;
+      __syncthreads();
+      if (P.part_mode == 0 && mq >= 15) {
+        if (threadIdx.x == 0) {
+          s_pwlo = s_spl[0];
+          fine_geometry(key_sub(s_spl[mq - 1], s_spl[0]), s_pwsh, s_pwlsh, s_pwcmax);
+          s_maxc = 0;
+        }
+        for (int k2 = threadIdx.x; k2 < mq; k2 += THREADS) dcnt[k2] = 0;
+        __syncthreads();
+        build_t1(s_spl, mq, s_pwlo, s_spl[mq - 1], s_pwsh, s_pwlsh, s_pwcmax, s_t1);
+        for (int i = threadIdx.x; i < S; i += THREADS)
+          atomicAdd(&dcnt[pw_digit(s[i], s_pwlo, s_pwsh, s_pwlsh, s_pwcmax, s_t1)], 1u);
+        __syncthreads();
+        for (int k2 = threadIdx.x; k2 < mq; k2 += THREADS) atomicMax(&s_maxc, dcnt[k2]);
+        __syncthreads();
+        pw = (unsigned)s_maxc * (unsigned)mq <= 2u * (unsigned)S + 4u * (unsigned)mq;
+      }
     }
     if (threadIdx.x == 0) {
-      list[p].L = (unsigned)Lf | (radix ? (0x100u | ((unsigned)dshift << 16)) : 0u) | (meff << 24);
+      list[p].L = (unsigned)Lf | (radix ? (0x100u | ((unsigned)dshift << 16)) : 0u) | (pw ? 0x200u : 0u) |
+                  (meff << 24);
       list[p].aux = dmul;
+      atomicAdd(&P.ctrl->modes[P.level < 8 ? P.level : 7][radix ? 1 : (pw ? 2 : 0)], 1u);
     }
     __syncthreads();
   }
@@ -855,7 +1061,10 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
         }
       }
     };
-    if (sizeof(W) == 8 && S.use_tree == 3) {
+    if (S.use_tree == 4) {
+      if (X.flt) count_tile(std::integral_constant<int, 4>{}, std::true_type{});
+      else count_tile(std::integral_constant<int, 4>{}, std::false_type{});
+    } else if (sizeof(W) == 8 && S.use_tree == 3) {
       if (X.flt) count_tile(std::integral_constant<int, 3>{}, std::true_type{});
       else count_tile(std::integral_constant<int, 3>{}, std::false_type{});
     } else if (S.use_tree >= 2) {
@@ -1216,7 +1425,8 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     const Xf<W> X = make_xf<W>(xf);
     // recompute child ids at write-out instead of staging them (cheap for
     // <= 32-bit words and for the 64-bit high-word classifier)
-    const bool radix = (sizeof(W) <= 4 && S.use_tree == 2) || (sizeof(W) == 8 && S.use_tree == 3);
+    const bool radix =
+        (sizeof(W) <= 4 && S.use_tree == 2) || (sizeof(W) == 8 && S.use_tree == 3) || S.use_tree == 4;
     auto classify_tile = [&](auto tree_tag, auto flt_tag) {
       constexpr int TREE = decltype(tree_tag)::value;
       constexpr bool FLT = decltype(flt_tag)::value;
@@ -1237,7 +1447,10 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
         }
       }
     };
-    if (sizeof(W) == 8 && S.use_tree == 3) {
+    if (S.use_tree == 4) {
+      if (X.flt) classify_tile(std::integral_constant<int, 4>{}, std::true_type{});
+      else classify_tile(std::integral_constant<int, 4>{}, std::false_type{});
+    } else if (sizeof(W) == 8 && S.use_tree == 3) {
       if (X.flt) classify_tile(std::integral_constant<int, 3>{}, std::true_type{});
       else classify_tile(std::integral_constant<int, 3>{}, std::false_type{});
     } else if (S.use_tree >= 2) {

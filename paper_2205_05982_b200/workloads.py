@@ -123,6 +123,20 @@ def make(name: str, n=None, seed=1, rank=0):
         return uniform_u64(n or 1_000_000, seed), "u64", False
     if name in ("c2-u32-asc", "c2-u32-desc"):
         return uniform_u32(n or 100_000_000, seed), "u32", name.endswith("desc")
+    if name.startswith("f32-normal"):  # (diagnostics) C2's f32 distribution, specials replaced / kept by kind
+        x = normal_f32_specials(n or 100_000_000, seed)
+        r = normal_f32_specials(1 << 20, seed + 99)
+        keep = name.split("-")[2] if name.count("-") == 2 else ""
+        bad = ~np.isfinite(x) | (x == 0)
+        if keep == "nan":
+            bad &= ~np.isnan(x)
+        elif keep == "zero":
+            bad &= x != 0
+        elif keep == "inf":
+            bad &= ~np.isinf(x)
+        r = r[np.isfinite(r) & (r != 0)]
+        x[bad] = r[: int(bad.sum())]
+        return x, "f32", False
     if name in ("c2-f32-asc", "c2-f32-desc"):
         return normal_f32_specials(n or 100_000_000, seed), "f32", name.endswith("desc")
     if name.startswith("c3") and len(name) == 3:
