@@ -182,6 +182,7 @@ struct Params {
   unsigned long long* seg;      // [cap_split + grid][kChildStride] per-(bucket p, CTA b) child
                                 //   counts (k_hist) -> absolute offsets (k_plan), slot p + b
   unsigned long long* childbase;  // [cap_split][kChildStride] absolute start of each child
+  unsigned short* tilecnt;      // [tiles][kChildStride] per-tile child counts (k_hist -> k_scatter)
   int grid;                     // CTAs of k_hist and k_scatter (identical tile ranges)
   Item* items[kNumLists];
   unsigned long long cap_split, cap_items;
@@ -977,13 +978,19 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
                  smem_raw + s * stage_bytes<W>(), &bars[s]);
     }
   }
-  for (int i = threadIdx.x; i < kChildStride; i += THREADS) hist[i] = 0;
+  for (int i = threadIdx.x; i < kChildStride + 1; i += THREADS) hist[i] = 0;
   __syncthreads();
   int p = s_p;
   SplitDesc d = list[p];
   unsigned long long p_next = p + 1 < nb ? list[p + 1].tile_base : ~0ull;  // next bucket's first tile
   int L = (int)(d.L & 0xFFu);
   load_splitters(P.splitters + (unsigned long long)p * 256, d.L, S, d.aux);
+  // this CTA's per-child totals of the current bucket (thread c owns children
+  // c*PER ..): the shared histogram is per tile, flushed to P.tilecnt
+  constexpr int PER = kChildStride / THREADS > 0 ? kChildStride / THREADS : 1;
+  unsigned ctot[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) ctot[j] = 0;
   unsigned phase = 0;
   int st = 0;  // stage of tile t
   for (unsigned long long t = t0; t < t1; ++t, st = st + 1 == Cfg<W>::kHistStages ? 0 : st + 1) {
@@ -998,9 +1005,11 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
       // flush and move to the next bucket
       const int nc = num_children(L);
       unsigned long long* sg = P.seg + (unsigned long long)(p + blockIdx.x) * kChildStride;
-      for (int c = threadIdx.x; c < nc; c += THREADS) {
-        sg[c] = hist[hslot(c)];
-        hist[hslot(c)] = 0;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int c = threadIdx.x * PER + j;
+        if (c < nc) sg[c] = ctot[j];
+        ctot[j] = 0;
       }
       while (p + 1 < nb && list[p + 1].tile_base <= t) ++p;
       d = list[p];
@@ -1082,11 +1091,30 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
       wide &= wide - 1;
       atomicAdd(&hist[hslot(classify_slow(enc<W>(lds_key<W>(kp, i * THREADS + threadIdx.x), xf), S))], 1u);  // rare
     }
-    __syncthreads();  // stage st fully consumed before it is refilled
+    __syncthreads();  // stage st fully consumed before it is refilled; tile counts complete
+    {
+      // the tile's child counts -> P.tilecnt (k_scatter places keys from
+      // them), into this CTA's totals, and the histogram is reset for the
+      // next tile (its first read follows that tile's barrier)
+      const int nc = num_children(L);
+      unsigned short* tc = P.tilecnt + t * kChildStride;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int c = threadIdx.x * PER + j;
+        const unsigned v = hist[hslot(c)];
+        hist[hslot(c)] = 0;
+        if (c < nc) tc[c] = (unsigned short)v;
+        ctot[j] += v;
+      }
+    }
   }
   const int nc = num_children(L);
   unsigned long long* sg = P.seg + (unsigned long long)(p + blockIdx.x) * kChildStride;
-  for (int c = threadIdx.x; c < nc; c += THREADS) sg[c] = hist[hslot(c)];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int c = threadIdx.x * PER + j;
+    if (c < nc) sg[c] = ctot[j];
+  }
 }
 
 // Column scan of the per-(bucket p, CTA b) child counts written by k_hist:
@@ -1344,8 +1372,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   constexpr int PER = kChildStride / THREADS > 0 ? kChildStride / THREADS : 1;  // children per thread
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned short* stage_b = reinterpret_cast<unsigned short*>(smem_raw + kStages * stage_bytes<W>());
-  constexpr int HC = Cfg<W>::kHistCopies;  // histogram copies (warp w uses copy w % HC)
-  unsigned* whist = reinterpret_cast<unsigned*>(stage_b + TILE);  // [HC][kChildStride]
+  unsigned* whist = reinterpret_cast<unsigned*>(stage_b + TILE);  // [kChildStride] per-child slot counters
   __shared__ SplSmem<W> S;
   __shared__ W* gptr[kChildStride];  // where staged slot 0 of child c goes (slot j -> gptr[c][j])
   __shared__ unsigned long long gcur[kChildStride];  // this CTA's next global slot per child
@@ -1385,8 +1412,6 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   };
   load_cursors();
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  unsigned* myhist = whist + (warp % HC) * kChildStride;
   const int out_xf = P.part_mode ? P.xf : XF_NONE;
   unsigned phase = 0;
   for (unsigned long long t = t0; t < t1; ++t) {
@@ -1406,8 +1431,17 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     }
     W* dst_buf = P.part_mode ? P.out : ((d.flags & F_IN_B) ? P.a : P.b);
     const int nc = num_children(L);
+    // this tile's child counts (k_hist measured them): issued before the
+    // tile wait so their latency hides under it
+    unsigned tcnt[PER];
+    {
+      const unsigned short* tc = P.tilecnt + t * kChildStride;
 #pragma unroll
-    for (int i = threadIdx.x; i < HC * kChildStride; i += THREADS) whist[i] = 0;
+      for (int j = 0; j < PER; ++j) {
+        const int c = threadIdx.x * PER + j;
+        tcnt[j] = c < nc ? (unsigned)tc[c] : 0u;
+      }
+    }
     const W* src = src_of(P, d.flags);
     const int xf = (d.flags & F_RAW) ? P.xf : XF_NONE;
     const unsigned long long lo = d.start + (t - d.tile_base) * TILE;
@@ -1418,13 +1452,13 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     mbar_wait(&bars[st], (phase >> st) & 1);
     phase ^= 1u << st;
     const unsigned char* kp = tile_fixup<W, THREADS>(src + lo, cnt, span, stage);
-    __syncthreads();  // tile complete in smem; whist zeroed
+    __syncthreads();  // tile complete in smem
     W k[ITEMS];
     int bk[ITEMS];
     unsigned wide = 0;
     const Xf<W> X = make_xf<W>(xf);
     // recompute child ids at write-out instead of staging them (cheap for
-    // <= 32-bit words and for the 64-bit high-word classifier)
+    // <= 32-bit words, the 64-bit high-word classifier and piecewise radix)
     const bool radix =
         (sizeof(W) <= 4 && S.use_tree == 2) || (sizeof(W) == 8 && S.use_tree == 3) || S.use_tree == 4;
     auto classify_tile = [&](auto tree_tag, auto flt_tag) {
@@ -1468,112 +1502,23 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       for (int i = 0; i < ITEMS; ++i)
         if (bk[i] == -1) bk[i] = classify_slow(k[i], S);
     }
-    // rank within (warp, child); bk[] becomes child << 16 | rank
-    bool same = bk[0] >= 0;
-#pragma unroll
-    for (int i = 1; i < ITEMS; ++i) same = same && bk[i] == bk[0];
-    const int b0 = __shfl_sync(0xffffffffu, bk[0], 0);
-    if (__all_sync(0xffffffffu, same && bk[0] == b0)) {
-      unsigned base = 0;
-      if (lane == 0) base = atomicAdd(&myhist[hslot(b0)], 32u * ITEMS);
-      base = __shfl_sync(0xffffffffu, base, 0) + lane * ITEMS;
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) bk[i] = (b0 << 16) | (int)(base + i);
-    } else if (cnt == TILE && __shfl_sync(0xffffffffu, bk[0], 31) == b0) {
-      // presorted-looking warp (its first 32-key slice is one child): rank
-      // slice by slice, one atomic per uniform slice -- 32 lanes would
-      // otherwise serialise on the same counter
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        const int ci = __shfl_sync(0xffffffffu, bk[i], 0);
-        if (__all_sync(0xffffffffu, bk[i] == ci)) {
-          unsigned base = 0;
-          if (lane == 0) base = atomicAdd(&myhist[hslot(ci)], 32u);
-          bk[i] = (ci << 16) | (int)(__shfl_sync(0xffffffffu, base, 0) + lane);
-        } else {
-          bk[i] = (bk[i] << 16) | (int)atomicAdd(&myhist[hslot(bk[i])], 1u);
-        }
-      }
-    } else if (cnt == TILE) {  // full tile: every id is valid (straight-line code)
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) bk[i] = (bk[i] << 16) | (int)atomicAdd(&myhist[hslot(bk[i])], 1u);
-    } else {
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i)
-        if (bk[i] >= 0) bk[i] = (bk[i] << 16) | (int)atomicAdd(&myhist[hslot(bk[i])], 1u);
-    }
-    __syncthreads();
-    // per child: exclusive prefix across warps, then across children; fold
-    // the child's tile offset into each warp's slot
+    // child offsets inside the tile (exclusive scan of the counts) become
+    // the children's slot counters; this CTA's private cursors give each
+    // child run its global place (no global atomics).  The scan's barriers
+    // also order every key read from the stage before the staging writes.
     {
-      unsigned tot[PER];
       unsigned sum = 0;
 #pragma unroll
-      for (int j = 0; j < PER; ++j) {
-        const int c = threadIdx.x * PER + j;
-        unsigned run = 0;
-#pragma unroll
-        for (int w = 0; w < HC; ++w) run += whist[w * kChildStride + hslot(c)];
-        tot[j] = run;
-        sum += run;
-      }
+      for (int j = 0; j < PER; ++j) sum += tcnt[j];
       unsigned total;
       unsigned ex = block_exclusive_scan<THREADS>(sum, &total, scan_scratch);
-      // reserve each child's global range now, consume the result only after
-      // staging so the atomic round trip overlaps the smem work
-      unsigned long long gres[PER];
-      unsigned exc[PER];
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
         const int c = threadIdx.x * PER + j;
-        unsigned run = ex;
-#pragma unroll
-        for (int w = 0; w < HC; ++w) {
-          const unsigned v = whist[w * kChildStride + hslot(c)];
-          whist[w * kChildStride + hslot(c)] = run;
-          run += v;
-        }
-        gres[j] = 0;
-        if (tot[j] && c < nc) {  // private cursor: no global atomics
-          gres[j] = gcur[c];
-          gcur[c] += tot[j];
-        }
-        exc[j] = ex;
-        ex += tot[j];
-      }
-      __syncthreads();
-      W* staged = reinterpret_cast<W*>(stage);
-      if (radix && cnt == TILE) {  // child ids are recomputed from the keys at write-out
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) staged[myhist[hslot(bk[i] >> 16)] + (unsigned)(bk[i] & 0xFFFF)] = k[i];
-      } else if (radix) {
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-          if (bk[i] >= 0) staged[myhist[hslot(bk[i] >> 16)] + (unsigned)(bk[i] & 0xFFFF)] = k[i];
-        }
-      } else if (cnt == TILE) {
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-          const int c = bk[i] >> 16;
-          const unsigned pos = myhist[hslot(c)] + (unsigned)(bk[i] & 0xFFFF);
-          staged[pos] = k[i];
-          stage_b[pos] = (unsigned short)c;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-          if (bk[i] >= 0) {
-            const int c = bk[i] >> 16;
-            const unsigned pos = myhist[hslot(c)] + (unsigned)(bk[i] & 0xFFFF);
-            staged[pos] = k[i];
-            stage_b[pos] = (unsigned short)c;
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < PER; ++j) {
-        const int c = threadIdx.x * PER + j;
-        if (tot[j] && c < nc) {
+        whist[hslot(c)] = ex;
+        if (tcnt[j]) {
+          const unsigned long long gres = gcur[c];
+          gcur[c] = gres + tcnt[j];
           // (vxs_partition_exchange: segment c/2 goes straight to its owner's
           // receive buffer at this rank's offset there -- the fused exchange)
           W* base = dst_buf;
@@ -1581,8 +1526,53 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
             const int sg = c >> 1;
             base = reinterpret_cast<W*>(P.xdst[sg]) + P.xoff[sg] - P.childbase[2 * sg];
           }
-          gptr[c] = base + ((long long)gres[j] - (long long)exc[j]);
+          gptr[c] = base + ((long long)gres - (long long)ex);
         }
+        ex += tcnt[j];
+      }
+    }
+    __syncthreads();  // slot counters and gptr ready
+    // stage the tile grouped by child: each key takes the next slot of its
+    // child (returning shared atomic); the tile's own TMA stage is reused
+    {
+      W* staged = reinterpret_cast<W*>(stage);
+      auto put = [&](unsigned pos, int i) {
+        staged[pos] = k[i];
+        if (!radix) stage_b[pos] = (unsigned short)bk[i];
+      };
+      bool same = bk[0] >= 0;
+#pragma unroll
+      for (int i = 1; i < ITEMS; ++i) same = same && bk[i] == bk[0];
+      const int b0 = __shfl_sync(0xffffffffu, bk[0], 0);
+      if (__all_sync(0xffffffffu, same && bk[0] == b0)) {
+        // the warp's whole sub-tile is one child: one atomic for 32*ITEMS keys
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(&whist[hslot(b0)], 32u * ITEMS);
+        base = __shfl_sync(0xffffffffu, base, 0) + lane * ITEMS;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) put(base + i, i);
+      } else if (cnt == TILE && __shfl_sync(0xffffffffu, bk[0], 31) == b0) {
+        // presorted-looking warp (its first 32-key slice is one child): slice
+        // by slice, one atomic per uniform slice -- 32 lanes would otherwise
+        // serialise on the same counter
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const int ci = __shfl_sync(0xffffffffu, bk[i], 0);
+          if (__all_sync(0xffffffffu, bk[i] == ci)) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(&whist[hslot(ci)], 32u);
+            put(__shfl_sync(0xffffffffu, base, 0) + lane, i);
+          } else {
+            put(atomicAdd(&whist[hslot(bk[i])], 1u), i);
+          }
+        }
+      } else if (cnt == TILE) {  // full tile: every id is valid (straight-line code)
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) put(atomicAdd(&whist[hslot(bk[i])], 1u), i);
+      } else {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i)
+          if (bk[i] >= 0) put(atomicAdd(&whist[hslot(bk[i])], 1u), i);
       }
     }
     W* staged = reinterpret_cast<W*>(stage);

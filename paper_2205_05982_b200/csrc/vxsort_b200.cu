@@ -208,7 +208,7 @@ int stream_grid() {
   return g < kMaxGrid ? g : kMaxGrid;
 }
 struct Layout {
-  size_t tmp, split0, split1, splitters, counts, childbase, seg, items[kNumLists], ctrl, total;
+  size_t tmp, split0, split1, splitters, counts, childbase, seg, tilecnt, items[kNumLists], ctrl, total;
   unsigned long long cap_split, cap_items;
 };
 
@@ -231,6 +231,9 @@ Layout layout_for(size_t n) {
   L.counts = take(L.cap_split * kChildStride * sizeof(unsigned long long));
   L.childbase = take(L.cap_split * kChildStride * sizeof(unsigned long long));
   L.seg = take((L.cap_split + kMaxGrid) * kChildStride * sizeof(unsigned long long));
+  // per-tile child counts of one level: at most n / Tile full tiles plus one
+  // partial tile per split bucket
+  L.tilecnt = take((n / Cfg<W>::kTile + L.cap_split + 1) * kChildStride * sizeof(unsigned short));
   for (int i = 0; i < kNumLists; ++i) L.items[i] = take(L.cap_items * sizeof(Item));
   L.ctrl = take(sizeof(Ctrl));
   L.total = off;
@@ -255,6 +258,7 @@ Params<W> make_params(W* keys, size_t n, int xf, uint64_t seed, unsigned char* w
   P.counts = reinterpret_cast<unsigned long long*>(ws + L.counts);
   P.seg = reinterpret_cast<unsigned long long*>(ws + L.seg);
   P.childbase = reinterpret_cast<unsigned long long*>(ws + L.childbase);
+  P.tilecnt = reinterpret_cast<unsigned short*>(ws + L.tilecnt);
   P.grid = stream_grid<W>();
   for (int i = 0; i < kNumLists; ++i) P.items[i] = reinterpret_cast<Item*>(ws + L.items[i]);
   P.cap_split = L.cap_split;
