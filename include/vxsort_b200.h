@@ -76,8 +76,9 @@ vxs_status vxs_sort_workspace_bytes(size_t n, vxs_key_type type, size_t* bytes);
 /* In-place sort of n keys at DEVICE pointer d_keys, stream-ordered on
  * `stream` (a cudaStream_t; NULL = legacy default stream).  d_workspace may
  * be NULL (then it is allocated stream-ordered).  The call synchronises the
- * stream once (to read the device bucket scheduler's level count); if stats
- * is non-NULL it is filled.  seed/has_seed mirror SortConfig.seed
+ * stream once (to read the device bucket scheduler's level count) unless the
+ * stream is being captured into a CUDA graph (see vxs_workspace_status); if
+ * stats is non-NULL it is filled.  seed/has_seed mirror SortConfig.seed
  * (vexsort.hpp:112-119): the output never depends on it. */
 vxs_status vxs_sort(void* d_keys, size_t n, vxs_key_type type, vxs_order order, uint64_t seed,
                     int has_seed, void* d_workspace, size_t workspace_bytes, void* stream,
@@ -218,6 +219,18 @@ vxs_status vxs_dist_last_counts(vxs_dist_ctx ctx, uint64_t* recv_per_rank, uint6
 vxs_status vxs_nccl_unique_id(void* id128);
 vxs_status vxs_nccl_comm_create(const void* id128, int world, int rank, void** comm);
 vxs_status vxs_nccl_comm_destroy(void* comm);
+
+/* CUDA graphs: vxs_sort / vxs_sort_range / vxs_argsort / vxs_sort_pairs on a
+ * stream under capture launch without any host round trip (the expected
+ * number of levels plus two guard levels -- an idle level exits at once --
+ * and every base-case class, item counts read on the device), so the call
+ * can be captured once and replayed.  Stats then hold only the launch count.
+ * vxs_workspace_status reads the device control block of the last sort that
+ * ran in d_workspace (n, type as for that sort): its stats, and
+ * VXS_INTERNAL if it overflowed a device list or (captured) needed more
+ * levels than were launched.  Synchronises `stream`. */
+vxs_status vxs_workspace_status(const void* d_workspace, size_t n, vxs_key_type type, void* stream,
+                                vxs_stats* stats);
 
 /* Key transform as used inside the kernels (exposed for tests): encodes
  * (inverse=0) or decodes (inverse=1) n keys in place on the device. */

@@ -27,7 +27,10 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libvxsort_b200.so")
+# VXSORT_LIB=checked loads the checked build (device-side bounds and
+# consistency checks, `make checked`); the default is the product build.
+LIB_PATH = os.path.join(_HERE, "lib", "libvxsort_b200_checked.so" if os.environ.get("VXSORT_LIB") == "checked"
+                        else "libvxsort_b200.so")
 
 KEY_TYPES = ["i16", "u16", "i32", "u32", "f32", "i64", "u64", "f64", "k128", "kv64"]
 KEY_CODE = {k: i for i, k in enumerate(KEY_TYPES)}
@@ -146,6 +149,8 @@ def lib():
         L.vxs_ipc_handle.argtypes = [vp, vp]
         L.vxs_ipc_open.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p)]
         L.vxs_ipc_close.argtypes = [vp]
+        L.vxs_workspace_status.argtypes = [vp, sz, i, vp, ctypes.POINTER(SortStats)]
+        L.vxs_workspace_status.restype = ctypes.c_int
         L.vxs_dist_create.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p)]
         L.vxs_dist_destroy.argtypes = [vp]
         L.vxs_dist_sort.argtypes = [vp, vp, sz, i, i, u64, i, ctypes.POINTER(ctypes.c_void_p),
@@ -173,7 +178,8 @@ EXPORTED_SYMBOLS = ["vxs_sort_workspace_bytes", "vxs_sort", "vxs_sort_host", "vx
                     "vxs_profile_reset", "vxs_profile_read", "vxs_partition_counts",
                     "vxs_partition_exchange", "vxs_device_alloc", "vxs_device_free", "vxs_ipc_handle",
                     "vxs_ipc_open", "vxs_ipc_close", "vxs_dist_create", "vxs_dist_destroy", "vxs_dist_sort",
-                    "vxs_dist_last_counts", "vxs_nccl_unique_id", "vxs_nccl_comm_create", "vxs_nccl_comm_destroy"]
+                    "vxs_dist_last_counts", "vxs_nccl_unique_id", "vxs_nccl_comm_create", "vxs_nccl_comm_destroy",
+                    "vxs_workspace_status"]
 
 
 class KernelProfile(ctypes.Structure):
@@ -508,6 +514,17 @@ def transform(keys, order: Order = Order.kAscending, inverse=False, key_type=Non
     with _device_of(keys):
         _check(lib().vxs_transform(keys.data_ptr(), _nkeys(keys, kt), KEY_CODE[kt], int(order),
                                    int(bool(inverse)), _stream_ptr(stream)))
+
+
+def workspace_status(workspace, n: int, key_type: str, stream=None) -> SortStats:
+    """Stats of the last sort that ran in ``workspace`` (e.g. a replayed CUDA
+    graph, whose captured call could not report them); raises if the device
+    scheduler flagged an error (vxs_workspace_status)."""
+    st = SortStats()
+    with _device_of(workspace):
+        _check(lib().vxs_workspace_status(workspace.data_ptr(), n, KEY_CODE[key_type], _stream_ptr(stream),
+                                          ctypes.byref(st)))
+    return st
 
 
 def base_case_capacity(key_type: str) -> int:

@@ -461,6 +461,7 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, W* 
     unsigned pos;
     if constexpr (RANK) pos = ((cnt[br[i] >> 17] >> h) & 0xFFFFu) + (br[i] & 0xFFFFu);
     else pos = (atomicAdd(&cnt[br[i] >> 17], 1u << h) >> h) & 0xFFFFu;
+    VXS_DCHECK(pos < (unsigned)TOTAL, "base case: bin slot outside the item");
     sk[BS::swz((int)pos)] = i * THREADS + tid < size ? k[i] : key_max<W>();
   }
   __syncthreads();

@@ -17,6 +17,27 @@
 //           lost and the inverse restores the exact input bits.
 #pragma once
 #include <cstdint>
+#include <cstdio>
+
+// Checked build (make checked -> lib/libvxsort_b200_checked.so, -DVXS_CHECKS):
+// device-side bounds and consistency checks on every index the kernels
+// compute (the analogue of the reference's bounds-checked scalar backend,
+// vec.hpp:85-120 / config.hpp:42-52).  A failed check prints where and traps
+// (the launch fails with a CUDA error).  Compiled out of the product build.
+#ifdef VXS_CHECKS
+#define VXS_DCHECK(cond, what)                                                                        \
+  do {                                                                                                \
+    if (!(cond)) {                                                                                    \
+      printf("vxsort check failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,        \
+             (int)blockIdx.x, (int)threadIdx.x);                                                     \
+      __trap();                                                                                       \
+    }                                                                                                 \
+  } while (0)
+#else
+#define VXS_DCHECK(cond, what) \
+  do {                         \
+  } while (0)
+#endif
 
 namespace vxs {
 

@@ -1089,7 +1089,9 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
     while (wide) {
       const int i = __ffs(wide) - 1;
       wide &= wide - 1;
-      atomicAdd(&hist[hslot(classify_slow(enc<W>(lds_key<W>(kp, i * THREADS + threadIdx.x), xf), S))], 1u);  // rare
+      const int b = classify_slow(enc<W>(lds_key<W>(kp, i * THREADS + threadIdx.x), xf), S);
+      VXS_DCHECK(b >= 0 && b < num_children(L), "k_hist: child id out of range");
+      atomicAdd(&hist[hslot(b)], 1u);  // rare
     }
     __syncthreads();  // stage st fully consumed before it is refilled; tile counts complete
     {
@@ -1241,6 +1243,7 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
     const unsigned long long cnt = c < nc ? P.counts[(unsigned long long)p * kChildStride + c] : 0ull;
     unsigned long long total;
     const unsigned long long off = block_exclusive_scan<THREADS>(cnt, &total, scan_scratch);
+    VXS_DCHECK(total == d.size, "k_plan: child counts do not add up to the bucket");
     if (c < nc) P.childbase[(unsigned long long)p * kChildStride + c] = d.start + off;
     s_cnt[c] = cnt;
     s_off[c] = off;
@@ -1512,6 +1515,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       for (int j = 0; j < PER; ++j) sum += tcnt[j];
       unsigned total;
       unsigned ex = block_exclusive_scan<THREADS>(sum, &total, scan_scratch);
+      VXS_DCHECK(total == (unsigned)cnt, "k_scatter: tile counts do not add up to the tile");
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
         const int c = threadIdx.x * PER + j;
@@ -1537,6 +1541,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     {
       W* staged = reinterpret_cast<W*>(stage);
       auto put = [&](unsigned pos, int i) {
+        VXS_DCHECK(pos < (unsigned)cnt, "k_scatter: staging slot outside the tile (k_hist/k_scatter counts differ)");
         staged[pos] = k[i];
         if (!radix) stage_b[pos] = (unsigned short)bk[i];
       };
@@ -1577,18 +1582,34 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     }
     W* staged = reinterpret_cast<W*>(stage);
     __syncthreads();
+#ifdef VXS_CHECKS
+    // every staged slot j of child c lands inside child c's range
+    auto chk = [&](int c, int j) {
+      VXS_DCHECK(c >= 0 && c < nc, "k_scatter: child id out of range");
+      const W* base = dst_buf;  // (exchange: the segment's place in its owner's window)
+      if (P.xchg) base = reinterpret_cast<const W*>(P.xdst[c >> 1]) + P.xoff[c >> 1] - P.childbase[2 * (c >> 1)];
+      const long long idx = (long long)((gptr[c] + j) - base);
+      const unsigned long long b0 = P.childbase[(unsigned long long)p * kChildStride + c];
+      const unsigned long long n0 = P.counts[(unsigned long long)p * kChildStride + c];
+      VXS_DCHECK(idx >= (long long)b0 && (unsigned long long)idx < b0 + n0, "k_scatter: key stored outside its child");
+    };
+#else
+    auto chk = [](int, int) {};
+#endif
     if (radix && out_xf == XF_NONE && cnt == TILE) {  // full tile: unrolled, no bounds
       const RadixReg<W> R(S);
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
         const int j = i * THREADS + threadIdx.x;
         const W v = staged[j];
+        chk(R.child(v), j);
         gptr[R.child(v)][j] = v;
       }
     } else if (out_xf == XF_NONE && cnt == TILE) {
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
         const int j = i * THREADS + threadIdx.x;
+        chk(stage_b[j], j);
         gptr[stage_b[j]][j] = staged[j];
       }
     } else if (radix) {
@@ -1596,6 +1617,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       if (out_xf == XF_NONE) {
         for (int j = threadIdx.x; j < cnt; j += THREADS) {
           const W v = staged[j];
+          chk(R.child(v), j);
           gptr[R.child(v)][j] = v;
         }
       } else {
@@ -1605,9 +1627,15 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
         }
       }
     } else if (out_xf == XF_NONE) {
-      for (int j = threadIdx.x; j < cnt; j += THREADS) gptr[stage_b[j]][j] = staged[j];
+      for (int j = threadIdx.x; j < cnt; j += THREADS) {
+        chk(stage_b[j], j);
+        gptr[stage_b[j]][j] = staged[j];
+      }
     } else {  // vxs_partition: decode into the caller's encoding
-      for (int j = threadIdx.x; j < cnt; j += THREADS) gptr[stage_b[j]][j] = dec<W>(staged[j], out_xf);
+      for (int j = threadIdx.x; j < cnt; j += THREADS) {
+        chk(stage_b[j], j);
+        gptr[stage_b[j]][j] = dec<W>(staged[j], out_xf);
+      }
     }
     __syncthreads();
   }
@@ -1648,6 +1676,8 @@ __global__ void __launch_bounds__(SortClass<CLS>::T, final_min_blocks<W, CLS>())
     if (it + gridDim.x < nitems) nxt = items[it + gridDim.x];
     const W* src = (item.flags & F_IN_B) ? P.b : P.a;
     const int size = (int)item.size;
+    VXS_DCHECK(item.size >= 1 && item.size <= (unsigned long long)(THREADS * ITEMS) && item.start + item.size <= P.n,
+               "k_final: item outside the array or its class");
     W k[ITEMS];
     // padding: the maximum for the network (class 0); a copy of the item's
     // first key for the counting sort (neutral for its min / max)

@@ -159,6 +159,9 @@ struct AsyncBuf {
   AsyncBuf& operator=(const AsyncBuf&) = delete;
   cudaError_t alloc(size_t bytes, cudaStream_t s) {
     st = s;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    if (cap == cudaStreamCaptureStatusActive) return cudaMallocAsync(&p, bytes, s);  // graph memory node
     return lib_malloc_async(&p, bytes, s);
   }
   cudaError_t free() {
@@ -368,6 +371,49 @@ void launch_final(Params<W>& P, unsigned long long count, cudaStream_t st) {
   fn<<<g, T, smem, st>>>(P);
 }
 
+// Graph-capture mode (run_sort): levels launched beyond the expected count,
+// and the base-case classes launched without host-side counts.
+constexpr int kCaptureGuardLevels = 2;
+
+#define VXS_CK_STATUS(expr)        \
+  do {                             \
+    const vxs_status s_ = (expr);  \
+    if (s_ != VXS_OK) return s_;   \
+  } while (0)
+
+// Unconverged split work after the last captured level -> error flag.
+template <typename W>
+__global__ void k_check_done(Params<W> P) {
+  if ((P.ctrl->split_packed[P.cur] >> 40) != 0) P.ctrl->error = 4;
+}
+
+template <typename W>
+int launch_final_all(Params<W>& P, cudaStream_t st) {
+  constexpr unsigned long long kAll = ~0ull;  // grid = occupancy; counts are read on the device
+  launch_final<W, 0>(P, kAll, st);
+  launch_final<W, 1>(P, kAll, st);
+  launch_final<W, 2>(P, kAll, st);
+  launch_final<W, 3>(P, kAll, st);
+  int launches = 4;
+  if constexpr (Cfg<W>::kCap >= 8192) {
+    launch_final<W, 4>(P, kAll, st);
+    ++launches;
+  }
+  {
+    auto fn = k_copy<W>;
+    const int g = grid_for((const void*)fn, 256, 0);
+    fn<<<g, 256, 0, st>>>(P);
+  }
+  {
+    constexpr int ITEMS = sizeof(W) >= 16 ? 8 : 16;
+    constexpr size_t smem = (size_t)padded_size<W>(SortClass<4>::T * ITEMS) * sizeof(W);
+    auto fn = k_final_fallback<W>;
+    const int g = grid_for((const void*)fn, SortClass<4>::T, smem);
+    fn<<<g, SortClass<4>::T, smem, st>>>(P);
+  }
+  return launches + 2;
+}
+
 // Control-block readback through mapped pinned memory written by a 1-warp
 // kernel: no copy engine involved, so the per-call sync never queues behind
 // a large D2H transfer on another stream (host pipeline, user copies).
@@ -474,6 +520,32 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
   int levels = 0;
   bool fallback = false;
   const int expect = expected_levels(n, Cfg<W>::kCap);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  VXS_CK(cudaStreamIsCapturing(st, &cap), "capture query");
+  if (cap == cudaStreamCaptureStatusActive) {
+    // Graph capture: no host round trip.  The expected levels plus
+    // kCaptureGuardLevels more are launched (a level with no split work
+    // exits at once), then every base-case class with an occupancy grid
+    // reading its item count on the device.  A sort that would need still
+    // more levels raises the control block's error flag instead
+    // (vxs_workspace_status reports it).
+    const int nlev = n > (size_t)Cfg<W>::kCap ? expect + kCaptureGuardLevels : 0;
+    for (int i = 0; i < nlev; ++i) {
+      P.level = i;
+      VXS_CK_STATUS(launch_level<W>(P, st, launches));
+      P.cur ^= 1;
+    }
+    k_check_done<W><<<1, 1, 0, st>>>(P);
+    ++launches;
+    launches += launch_final_all<W>(P, st);
+    VXS_CK(cudaGetLastError(), "capture launches");
+    VXS_CK(owned.free(), "workspace free");
+    if (stats) {
+      stats->max_depth = (size_t)nlev;
+      stats->kernel_launches = launches;
+    }
+    return VXS_OK;
+  }
   if (n > (size_t)Cfg<W>::kCap) {
     int batch = expect;
     for (;;) {
@@ -1304,6 +1376,32 @@ vxs_status vxs_sort(void* d_keys, size_t n, vxs_key_type type, vxs_order order, 
     using W = std::remove_pointer_t<decltype(tag)>;
     return run_sort<W>(static_cast<W*>(d_keys), n, xf, s, d_workspace, workspace_bytes,
                        static_cast<cudaStream_t>(stream), stats);
+  });
+}
+
+vxs_status vxs_workspace_status(const void* d_workspace, size_t n, vxs_key_type type, void* stream,
+                                vxs_stats* stats) {
+  if (!d_workspace) return fail(VXS_INVALID_ARGUMENT, "vxsort_b200: workspace is NULL");
+  return with_word(type, [&](auto* tag) -> vxs_status {
+    using W = std::remove_pointer_t<decltype(tag)>;
+    const Layout L = layout_for<W>(n);
+    Ctrl h{};
+    VXS_CK_STATUS(read_ctrl(reinterpret_cast<const Ctrl*>(static_cast<const unsigned char*>(d_workspace) + L.ctrl), h,
+                            static_cast<cudaStream_t>(stream)));
+    if (stats) {
+      std::memset(stats, 0, sizeof(*stats));
+      int lv = 0;
+      for (int l = 0; l < 8; ++l)
+        if (h.modes[l][0] + h.modes[l][1] + h.modes[l][2]) lv = l + 1;
+      stats->max_depth = (size_t)lv;
+      stats->partition_calls = (size_t)h.partition_calls;
+      stats->base_case_calls = (size_t)h.base_cases;
+      stats->keys_partitioned = (size_t)h.keys_partitioned;
+      stats->workspace_bytes = L.total;
+    }
+    if (h.error) return fail(VXS_INTERNAL, h.error == 4 ? "vxsort_b200: captured sort needed more levels than launched"
+                                                        : "vxsort_b200: device scheduler list overflow");
+    return VXS_OK;
   });
 }
 
