@@ -349,6 +349,17 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, W* 
   block_minmax<W, THREADS, ITEMS>(k, lo, hi, red_lo, red_hi);  // (its barrier covers cnt)
   const int bl = key_bitlen(key_sub(hi, lo));
   const int shift = bl > BS::kNBBits ? bl - BS::kNBBits : 0;
+  // 64-bit keys whose high words differ: lo has a zero low word (block_minmax),
+  // so (k - lo) >> shift with shift >= 32 is (hi(k) - hi(lo)) >> (shift - 32)
+  // exactly -- two 32-bit ops instead of a 64-bit subtract and shift
+  const bool hiword = sizeof(W) == 8 && shift >= 32;  // (block-uniform)
+  auto bin_of = [&](const W& x) -> unsigned {
+    if constexpr (sizeof(W) == 8) {
+      if (hiword)
+        return ((unsigned)((unsigned long long)x >> 32) - (unsigned)((unsigned long long)lo >> 32)) >> (shift - 32);
+    }
+    return key_shr32(key_sub(x, lo), shift);
+  };
   // pass 1: count.  br[i] = counter word << 17 | half << 16 (| rank, RANK)
   unsigned br[ITEMS];
   unsigned sq = 0;  // sum over bins of count^2 (the cost of the rounds)
@@ -356,7 +367,7 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, W* 
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const bool valid = i * THREADS + tid < size;
-    const unsigned b = valid ? key_shr32(key_sub(k[i], lo), shift) : (unsigned)(NB + BS::kBinsPerWord);
+    const unsigned b = valid ? bin_of(k[i]) : (unsigned)(NB + BS::kBinsPerWord);
     const int w = BS::kPacked ? BS::wslot((int)(b >> 1)) : BS::wslot((int)b);
     const unsigned h = BS::kPacked ? (b & 1u) << 4 : 0u;
     br[i] = ((unsigned)w << 17) | ((h >> 4) << 16);
