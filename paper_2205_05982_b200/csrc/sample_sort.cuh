@@ -357,11 +357,16 @@ __device__ __forceinline__ void fine_geometry(const W& range, int& rsh, int& lsh
   cmax = key_shr32(range, rsh);
 }
 
+// (first, end) splitter pair of key x's table cell.  A first-level bucket
+// with a single cell (<= 1 splitter: the common case for smooth splitter
+// sets) keeps its pair in t1 itself (bit 20 set): one table load per key.
+constexpr unsigned kT1Direct = 1u << 20;
 template <typename W>
-__device__ __forceinline__ unsigned lut_cell(const W& x, const SplSmem<W>& S) {
+__device__ __forceinline__ unsigned lut_pair(const W& x, const SplSmem<W>& S) {
   const unsigned cf = fine_unit(x, S.lo, S.shift, S.lshift, S.cmax);
   const unsigned t = S.t1[cf >> kSubBits];
-  return (t & 0xFFFFu) + ((cf & ((1u << kSubBits) - 1)) >> (kSubBits - (t >> 16)));
+  if (t & kT1Direct) return t & 0xFFFFu;
+  return S.lut[(t & 0xFFFFu) + ((cf & ((1u << kSubBits) - 1)) >> (kSubBits - (t >> 16)))];
 }
 
 template <typename W>
@@ -550,6 +555,9 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, unsigned lraw, Sp
     }
     __syncthreads();
   }
+  // single-cell buckets: their (first, end) pair goes straight into t1
+  for (int j = threadIdx.x; j < n1; j += blockDim.x)
+    if ((S.t1[j] >> 16) == 0) S.t1[j] = (unsigned)S.lut[S.t1[j] & 0xFFFFu] | kT1Direct;
   if (wide) atomicAdd(&s_wide, wide);
   __syncthreads();
   const bool tree = s_wide > 8;  // (block-uniform)
@@ -592,7 +600,7 @@ __device__ __forceinline__ int classify_mode(const W& x, const SplSmem<W>& S) {
     // Cell c holds splitters [i, e).  e == i: answer i, no equality possible
     // (srt[i] >= end of cell > x).  e == i+1: one compare with srt[i] gives
     // the answer and the equality bit.  Wider cells take the slow path.
-    const unsigned pr = S.lut[lut_cell(x, S)];
+    const unsigned pr = lut_pair(x, S);
     const int i = (int)(pr & 0xFFu);
     const int e = (int)(pr >> 8);
     const W sp = S.srt[i];
@@ -642,7 +650,7 @@ __device__ __forceinline__ int classify_fast(const W& x, const SplSmem<W>& S) {
 
 template <typename W>
 __device__ __noinline__ int classify_slow(const W& x, const SplSmem<W>& S) {
-  const unsigned pr = S.lut[lut_cell(x, S)];
+  const unsigned pr = lut_pair(x, S);
   const int i = lower_bound_smem(S.srt, (int)(pr & 0xFFu), (int)(pr >> 8), x);
   const int eq = (i < S.m && key_eq(S.srt[i], x)) ? 1 : 0;
   return 2 * i + eq;
