@@ -302,12 +302,16 @@ __device__ __forceinline__ unsigned radix_digit(unsigned long long x, unsigned l
   const unsigned long long f = ((x > lo ? x : lo) - lo) >> shift;
   return umin(__umulhi((f >> 32) ? 0xFFFFFFFFu : (unsigned)f, mul), m);
 }
-// 64-bit keys whose bucket range spans >= 56 bits (shift >= 32): only the
-// high word of x - lo matters, and it never needs saturation.
+// 64-bit keys whose bucket range spans >= 56 bits (shift >= 32): the digit
+// is taken from the high words alone, hi(x) - hi(lo) (32-bit ops; never
+// saturates).  It can differ from the exact (x - lo) >> shift by one unit
+// before the shift where lo(x) < lo(lo) -- still monotone in x, and every
+// kernel uses this same function, so the split stays consistent.
 __device__ __forceinline__ unsigned radix_digit_hi(unsigned long long x, unsigned long long lo, int shift,
                                                    unsigned mul, unsigned m) {
-  const unsigned f = (unsigned)((x - lo) >> 32) >> (shift - 32);
-  return umin(__umulhi(x < lo ? 0u : f, mul), m);
+  const unsigned xh = (unsigned)(x >> 32), lh = (unsigned)(lo >> 32);
+  const unsigned f = (xh - lh) >> (shift - 32);
+  return umin(__umulhi(xh < lh ? 0u : f, mul), m);
 }
 __device__ __forceinline__ unsigned radix_digit(const U128& x, const U128& lo, int shift, unsigned mul, unsigned m) {
   if (key_lt(x, lo)) return 0u;
@@ -1424,6 +1428,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   load_cursors();
   const int lane = threadIdx.x & 31;
   const int out_xf = P.part_mode ? P.xf : XF_NONE;
+  const bool xchg = P.xchg != 0;
   unsigned phase = 0;
   for (unsigned long long t = t0; t < t1; ++t) {
     const int st = (int)((t - t0) & (kStages - 1));
@@ -1534,7 +1539,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
           // (vxs_partition_exchange: segment c/2 goes straight to its owner's
           // receive buffer at this rank's offset there -- the fused exchange)
           W* base = dst_buf;
-          if (P.xchg) {
+          if (xchg) {
             const int sg = c >> 1;
             base = reinterpret_cast<W*>(P.xdst[sg]) + P.xoff[sg] - P.childbase[2 * sg];
           }

@@ -594,7 +594,8 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
     const bool copy = h.item_count[kListCopySmall] || h.item_count[kListCopyBig];
     int others = copy ? 1 : 0;
     for (int c = 0; c < kNumSortClasses; ++c) others += (c != main_cls && h.item_count[c]) ? 1 : 0;
-    SideStream* ss = others ? side_stream() : nullptr;
+    static const bool serial = std::getenv("VXSORT_SERIAL_CLASSES") != nullptr;  // (diagnostics)
+    SideStream* ss = (others && !serial) ? side_stream() : nullptr;
     cudaStream_t sd = ss ? ss->s : st;
     if (ss) {
       VXS_CK(cudaEventRecord(ss->fork, st), "fork");
