@@ -184,6 +184,7 @@ struct Params {
   unsigned long long* childbase;  // [cap_split][kChildStride] absolute start of each child
   unsigned short* tilecnt;      // [tiles][kChildStride] per-tile child counts (k_hist -> k_scatter)
   int grid;                     // CTAs of k_hist and k_scatter (identical tile ranges)
+  int root_init;                // k_sample sets up the root bucket (level-0 launch; see k_sample)
   Item* items[kNumLists];
   unsigned long long cap_split, cap_items;
   W* out;                       // part_mode output
@@ -682,8 +683,7 @@ __device__ __forceinline__ int find_bucket(const SplitDesc* list, int nb, unsign
 // Root setup: reset counters; the whole array becomes one split bucket or one
 // base-case item (driver.hpp:172-191's n<=1 / n<=256 / recurse dispatch).
 template <typename W>
-__global__ void k_init(Params<W> P) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ __forceinline__ void init_root(const Params<W>& P) {
   Ctrl* c = P.ctrl;
   c->split_packed[0] = 0;
   c->split_packed[1] = 0;
@@ -713,6 +713,12 @@ __global__ void k_init(Params<W> P) {
   }
 }
 
+template <typename W>
+__global__ void k_init(Params<W> P) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  init_root(P);
+}
+
 // Splitter selection (replaces choose_pivot, pivot.hpp:146-172): stratified
 // random 4-key chunks (cache-line friendly like the reference's 64-B chunks,
 // PAPER.md:393-398), smem bitonic sort, equidistant splitters.
@@ -730,7 +736,15 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
   __shared__ unsigned s_pwcmax;
   __shared__ W s_red_lo[THREADS / 32];
   __shared__ W s_red_hi[THREADS / 32];
-  const unsigned long long packed = P.ctrl->split_packed[P.cur];
+  // P.root_init (the level-0 launch of a sort with n > Cap): the root
+  // bucket is set up here by CTA 0 (k_init's work, one launch fewer); the
+  // level has exactly that one bucket
+  if (P.root_init) {
+    if (blockIdx.x != 0) return;
+    if (threadIdx.x == 0) init_root(P);
+    __syncthreads();
+  }
+  const unsigned long long packed = P.root_init ? (1ull << 40) : P.ctrl->split_packed[P.cur];
   const int nb = (int)(packed >> 40);
   if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrl->split_packed[P.cur ^ 1] = 0;
   SplitDesc* list = P.split[P.cur];
@@ -1251,8 +1265,25 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
     const int L = (int)(d.L & 0xFFu);
     const int nc = num_children(L);
     const int c = threadIdx.x;
-    // per-child totals were reduced over the touching CTAs by k_segscan
-    const unsigned long long cnt = c < nc ? P.counts[(unsigned long long)p * kChildStride + c] : 0ull;
+    unsigned long long cnt = 0;
+    if (P.level == 0) {
+      // the root's per-child totals were reduced over every CTA row by k_segscan_root
+      cnt = c < nc ? P.counts[(unsigned long long)p * kChildStride + c] : 0ull;
+    } else if (c < nc) {
+      // column scan of child c over the CTA rows touching this bucket (a
+      // handful below the root): row slots become offsets, the sum the total
+      const unsigned long long T = P.ctrl->split_packed[P.cur] & kTileMask;
+      const unsigned long long tpc = (T + P.grid - 1) / P.grid;
+      const int b_first = (int)(d.tile_base / tpc);
+      const int b_last = (int)((d.tile_base + (unsigned long long)ntiles_dev<W>(d.size) - 1) / tpc);
+      for (int b = b_first; b <= b_last; ++b) {
+        unsigned long long* sl = P.seg + (unsigned long long)(p + b) * kChildStride + c;
+        const unsigned long long v = *sl;
+        *sl = cnt;
+        cnt += v;
+      }
+      P.counts[(unsigned long long)p * kChildStride + c] = cnt;
+    }
     unsigned long long total;
     const unsigned long long off = block_exclusive_scan<THREADS>(cnt, &total, scan_scratch);
     VXS_DCHECK(total == d.size, "k_plan: child counts do not add up to the bucket");

@@ -333,15 +333,9 @@ vxs_status launch_level(Params<W>& P, cudaStream_t st, int& launches) {
     auto fn = k_hist<W>;
     pdl_launch(fn, P.grid, Cfg<W>::kHistThreads, hist_smem<W>(), st, P);
   }
-  {
+  if (P.level == 0) {  // the root bucket: every CTA holds a row (deeper levels: k_plan scans)
     ProfScope ps(K_SEGSCAN + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
-    if (P.level == 0) {  // the root bucket: every CTA holds a row
-      pdl_launch(k_segscan_root<W>, (kChildStride + 31) / 32, 1024, 0, st, P);
-    } else {
-      auto fn = k_segscan<W>;
-      const int g = grid_for((const void*)fn, 128, 0);
-      pdl_launch(fn, g, 128, 0, st, P);
-    }
+    pdl_launch(k_segscan_root<W>, (kChildStride + 31) / 32, 1024, 0, st, P);
   }
   {
     ProfScope ps(K_PLAN + K_COUNT * (1 + (P.level < 7 ? P.level : 7)), st);
@@ -354,7 +348,8 @@ vxs_status launch_level(Params<W>& P, cudaStream_t st, int& launches) {
     auto fn = k_scatter<W>;
     pdl_launch(fn, P.grid, Cfg<W>::kScatThreads, scatter_smem<W>(), st, P);
   }
-  launches += 5;
+  launches += P.level == 0 ? 5 : 4;
+  P.root_init = 0;  // (only the first level's k_sample sets up the root)
   VXS_CK(cudaGetLastError(), "level launch");
   return VXS_OK;
 }
@@ -511,11 +506,13 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
   P.rlo = rlo;
   P.rhi = std::min(rhi, n);
   int launches = 0;
-  {
+  if (n > (size_t)Cfg<W>::kCap) {
+    P.root_init = 1;  // the first k_sample sets up the root bucket
+  } else {
     ProfScope ps(K_INIT, st);
     k_init<W><<<1, 32, 0, st>>>(P);
+    ++launches;
   }
-  ++launches;
   Ctrl h{};
   int levels = 0;
   bool fallback = false;
