@@ -491,6 +491,7 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, W* 
     for (unsigned r = 0; r < rounds; r += 2) {
 #pragma unroll
       for (int i = 0; i + 1 < ITEMS; i += 2) cas(v[i], v[i + 1]);
+      if (r + 1 >= rounds) break;  // odd largest bin: its last round is an even one (block-uniform)
 #pragma unroll
       for (int i = 1; i + 1 < ITEMS; i += 2) cas(v[i], v[i + 1]);
       const W nx = shfl_next(v[0]);
