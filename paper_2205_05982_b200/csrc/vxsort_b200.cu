@@ -1383,6 +1383,11 @@ vxs_status vxs_workspace_status(const void* d_workspace, size_t n, vxs_key_type 
   return with_word(type, [&](auto* tag) -> vxs_status {
     using W = std::remove_pointer_t<decltype(tag)>;
     const Layout L = layout_for<W>(n);
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    if (n <= 1) {  // a sort of <= 1 key never touches the workspace (run_sort)
+      if (stats) stats->workspace_bytes = L.total;
+      return VXS_OK;
+    }
     Ctrl h{};
     VXS_CK_STATUS(read_ctrl(reinterpret_cast<const Ctrl*>(static_cast<const unsigned char*>(d_workspace) + L.ctrl), h,
                             static_cast<cudaStream_t>(stream)));
