@@ -454,6 +454,7 @@ __device__ __forceinline__ unsigned block_scan_small(unsigned* v, int count, uns
 // [256, 512), so the hot counters are consecutive words over all 32 banks
 // instead of every other bank.
 __host__ __device__ __forceinline__ int hslot(int c) { return (c >> 1) | ((c & 1) << 8); }
+__host__ __device__ __forceinline__ int unslot(int s) { return ((s & 255) << 1) | (s >> 8); }
 
 // Children of a bucket with m splitters: ids 0..2m+1 (the last one is the
 // equality bucket of the maximum key, used when the tree pads with it).
@@ -638,10 +639,11 @@ struct RadixReg {
   __device__ __forceinline__ explicit RadixReg(const SplSmem<W>& S)
       : lo(S.lo), shift(S.shift), m((unsigned)S.m), mul(S.mul), cmax(S.cmax), lshift(S.lshift), t1(S.t1),
         pw(S.use_tree == 4) {}
-  __device__ __forceinline__ int child(const W& x) const {
-    if (pw) return 2 * (int)pw_digit(x, lo, shift, lshift, cmax, t1);
-    if constexpr (sizeof(W) == 8) return 2 * (int)radix_digit_hi(x, lo, shift, mul, m);  // (mode 3 only)
-    else return 2 * (int)radix_digit(x, lo, shift, mul, m);
+  // shared-histogram slot of x's child (= its digit: radix children are even, hslot(2d) = d)
+  __device__ __forceinline__ int slot(const W& x) const {
+    if (pw) return (int)pw_digit(x, lo, shift, lshift, cmax, t1);
+    if constexpr (sizeof(W) == 8) return (int)radix_digit_hi(x, lo, shift, mul, m);  // (mode 3 only)
+    else return (int)radix_digit(x, lo, shift, mul, m);
   }
 };
 
@@ -1057,18 +1059,44 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
     __syncthreads();
     unsigned wide = 0;  // items whose cell holds > 2 splitters (rare)
     const Xf<W> X = make_xf<W>(xf);
+    // full tiles of <= 8-byte keys are read in 16-byte chunks (TileVec layout)
+    constexpr bool kVec = sizeof(W) <= 8;
+    const TileVec<W, THREADS> tv(src + lo, span, stage, kp);
     auto count_tile = [&](auto tree_tag, auto flt_tag) {
       constexpr int TREE = decltype(tree_tag)::value;
       constexpr bool FLT = decltype(flt_tag)::value;
       if (cnt == TILE && TREE >= 2) {  // radix: stream classify -> count
+        if constexpr (kVec) {  // 16-byte key loads, KPC independent classify chains per load
+          constexpr int KPC = TileVec<W, THREADS>::KPC;
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i)
-          atomicAdd(&hist[hslot(classify_mode<TREE>(enc_x<FLT>(lds_key<W>(kp, i * THREADS + threadIdx.x), X), S))], 1u);
+          for (int q = 0; q < ITEMS / KPC; ++q) {
+            W kk[KPC];
+            tv.load(q, kk);
+#pragma unroll
+            for (int e = 0; e < KPC; ++e)
+              atomicAdd(&hist[hslot(classify_mode<TREE>(enc_x<FLT>(kk[e], X), S))], 1u);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < ITEMS; ++i)
+            atomicAdd(&hist[hslot(classify_mode<TREE>(enc_x<FLT>(lds_key<W>(kp, i * THREADS + threadIdx.x), X), S))], 1u);
+        }
       } else if (cnt == TILE) {
         int bk[ITEMS];
+        if constexpr (kVec) {
+          constexpr int KPC = TileVec<W, THREADS>::KPC;
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i)
-          bk[i] = classify_mode<TREE>(enc_x<FLT>(lds_key<W>(kp, i * THREADS + threadIdx.x), X), S);
+          for (int q = 0; q < ITEMS / KPC; ++q) {
+            W kk[KPC];
+            tv.load(q, kk);
+#pragma unroll
+            for (int e = 0; e < KPC; ++e) bk[q * KPC + e] = classify_mode<TREE>(enc_x<FLT>(kk[e], X), S);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < ITEMS; ++i)
+            bk[i] = classify_mode<TREE>(enc_x<FLT>(lds_key<W>(kp, i * THREADS + threadIdx.x), X), S);
+        }
         // a warp whose whole sub-tile is one child (low-entropy input) adds
         // once instead of 32*ITEMS same-address atomics
         bool same = bk[0] >= 0;
@@ -1115,7 +1143,8 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
     while (wide) {
       const int i = __ffs(wide) - 1;
       wide &= wide - 1;
-      const int b = classify_slow(enc<W>(lds_key<W>(kp, i * THREADS + threadIdx.x), xf), S);
+      const int b =
+          classify_slow(enc<W>(lds_key<W>(kp, (kVec && cnt == TILE) ? tv.index(i) : i * THREADS + threadIdx.x), xf), S);
       VXS_DCHECK(b >= 0 && b < num_children(L), "k_hist: child id out of range");
       atomicAdd(&hist[hslot(b)], 1u);  // rare
     }
@@ -1397,6 +1426,40 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
     }
     __syncthreads();
   }
+  // Per-tile child counts (k_hist) -> exclusive prefixes in place, one warp
+  // per tile (lane l owns children 16l .. 16l+15: two 16-byte loads, a warp
+  // scan, two stores).  k_scatter then starts every tile from its prefixes
+  // instead of a block-wide scan (three barriers per tile fewer).  Entries
+  // past the bucket's child count hold stale values; prefixes are causal, so
+  // the entries k_scatter reads (<= child count) are exact.
+  {
+    const unsigned long long T = packed & kTileMask;
+    const int lane = threadIdx.x & 31;
+    const unsigned long long nw = (unsigned long long)gridDim.x * (THREADS / 32);
+    for (unsigned long long t = (unsigned long long)blockIdx.x * (THREADS / 32) + (threadIdx.x >> 5); t < T; t += nw) {
+      uint4* row = reinterpret_cast<uint4*>(P.tilecnt + t * kChildStride) + 2 * lane;
+      uint4 q[2] = {row[0], row[1]};
+      unsigned* w = reinterpret_cast<unsigned*>(q);  // 8 words = 16 u16 counts
+      unsigned sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sum += (w[j] & 0xFFFFu) + (w[j] >> 16);
+      unsigned incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      unsigned run = incl - sum;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const unsigned a = w[j] & 0xFFFFu, b = w[j] >> 16;
+        w[j] = (run & 0xFFFFu) | ((run + a) << 16);
+        run += a + b;
+      }
+      row[0] = q[0];
+      row[1] = q[1];
+    }
+  }
 }
 
 // Scatter: classify again (radix digit / table / tree), count per child
@@ -1422,7 +1485,6 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   __shared__ SplSmem<W> S;
   __shared__ W* gptr[kChildStride];  // where staged slot 0 of child c goes (slot j -> gptr[c][j])
   __shared__ unsigned long long gcur[kChildStride];  // this CTA's next global slot per child
-  __shared__ unsigned scan_scratch[32];
   __shared__ __align__(8) unsigned long long bars[kStages];
   __shared__ int s_p;
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
@@ -1478,22 +1540,23 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     }
     W* dst_buf = P.part_mode ? P.out : ((d.flags & F_IN_B) ? P.a : P.b);
     const int nc = num_children(L);
-    // this tile's child counts (k_hist measured them): issued before the
-    // tile wait so their latency hides under it
-    unsigned tcnt[PER];
-    {
-      const unsigned short* tc = P.tilecnt + t * kChildStride;
-#pragma unroll
-      for (int j = 0; j < PER; ++j) {
-        const int c = threadIdx.x * PER + j;
-        tcnt[j] = c < nc ? (unsigned)tc[c] : 0u;
-      }
-    }
     const W* src = src_of(P, d.flags);
     const int xf = (d.flags & F_RAW) ? P.xf : XF_NONE;
     const unsigned long long lo = d.start + (t - d.tile_base) * TILE;
     const unsigned long long end = d.start + d.size;
     const int cnt = (int)((end - lo) < (unsigned long long)TILE ? (end - lo) : TILE);
+    // this tile's child prefixes (k_hist counted, k_plan scanned): issued
+    // before the tile wait so their latency hides under it.  tpre[j] = first
+    // staging slot of child tid*PER + j; tpre[PER] = end of the last one.
+    unsigned tpre[PER + 1];
+    {
+      const unsigned short* tc = P.tilecnt + t * kChildStride;
+#pragma unroll
+      for (int j = 0; j <= PER; ++j) {
+        const int c = threadIdx.x * PER + j;
+        tpre[j] = c < nc ? (unsigned)tc[c] : (unsigned)cnt;
+      }
+    }
     const TileSpan span = tile_span(src + lo, (unsigned long long)cnt * sizeof(W));
     unsigned char* stage = smem_raw + st * stage_bytes<W>();
     mbar_wait(&bars[st], (phase >> st) & 1);
@@ -1508,22 +1571,45 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     // <= 32-bit words, the 64-bit high-word classifier and piecewise radix)
     const bool radix =
         (sizeof(W) <= 4 && S.use_tree == 2) || (sizeof(W) == 8 && S.use_tree == 3) || S.use_tree == 4;
+    // bk[] holds each key's shared-histogram SLOT (hslot of its child id; the
+    // digit itself in the radix modes), or -1 (wide cell) / -2 (past the tile)
     auto classify_tile = [&](auto tree_tag, auto flt_tag) {
       constexpr int TREE = decltype(tree_tag)::value;
       constexpr bool FLT = decltype(flt_tag)::value;
+      auto to_slot = [](int id) {
+        if constexpr (TREE >= 2) return id >> 1;  // (even ids: folds to the digit)
+        else return id >= 0 ? hslot(id) : id;
+      };
       if (cnt == TILE) {  // full tile: no per-key bounds (branch-free classify)
+        if constexpr (sizeof(W) <= 8) {  // 16-byte key loads (TileVec layout; any key -> item map works)
+          constexpr int KPC = TileVec<W, THREADS>::KPC;
+          const TileVec<W, THREADS> tv(src + lo, span, stage, kp);
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-          k[i] = enc_x<FLT>(lds_key<W>(kp, i * THREADS + threadIdx.x), X);
-          bk[i] = classify_mode<TREE>(k[i], S);
-          if (bk[i] == -1) wide |= 1u << i;
+          for (int q = 0; q < ITEMS / KPC; ++q) {
+            W kk[KPC];
+            tv.load(q, kk);
+#pragma unroll
+            for (int e = 0; e < KPC; ++e) {
+              const int i = q * KPC + e;
+              k[i] = enc_x<FLT>(kk[e], X);
+              bk[i] = to_slot(classify_mode<TREE>(k[i], S));
+              if (bk[i] == -1) wide |= 1u << i;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < ITEMS; ++i) {
+            k[i] = enc_x<FLT>(lds_key<W>(kp, i * THREADS + threadIdx.x), X);
+            bk[i] = to_slot(classify_mode<TREE>(k[i], S));
+            if (bk[i] == -1) wide |= 1u << i;
+          }
         }
       } else {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
           const int idx = i * THREADS + threadIdx.x;
           k[i] = idx < cnt ? enc_x<FLT>(lds_key<W>(kp, idx), X) : key_max<W>();
-          bk[i] = idx < cnt ? classify_mode<TREE>(k[i], S) : -2;
+          bk[i] = idx < cnt ? to_slot(classify_mode<TREE>(k[i], S)) : -2;
           if (bk[i] == -1) wide |= 1u << i;
         }
       }
@@ -1547,26 +1633,22 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     if (wide) {  // rare; static indices keep k[] / bk[] in registers
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i)
-        if (bk[i] == -1) bk[i] = classify_slow(k[i], S);
+        if (bk[i] == -1) bk[i] = hslot(classify_slow(k[i], S));
     }
-    // child offsets inside the tile (exclusive scan of the counts) become
-    // the children's slot counters; this CTA's private cursors give each
-    // child run its global place (no global atomics).  The scan's barriers
-    // also order every key read from the stage before the staging writes.
+    // child offsets inside the tile (the prefixes k_plan scanned) become the
+    // children's slot counters; this CTA's private cursors give each child
+    // run its global place (no global atomics).
     {
-      unsigned sum = 0;
-#pragma unroll
-      for (int j = 0; j < PER; ++j) sum += tcnt[j];
-      unsigned total;
-      unsigned ex = block_exclusive_scan<THREADS>(sum, &total, scan_scratch);
-      VXS_DCHECK(total == (unsigned)cnt, "k_scatter: tile counts do not add up to the tile");
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
         const int c = threadIdx.x * PER + j;
+        const unsigned ex = tpre[j], tcnt = tpre[j + 1] - tpre[j];
+        VXS_DCHECK(tpre[j] <= tpre[j + 1] && tpre[j + 1] <= (unsigned)cnt,
+                   "k_scatter: tile prefixes do not fit the tile");
         whist[hslot(c)] = ex;
-        if (tcnt[j]) {
+        if (tcnt) {
           const unsigned long long gres = gcur[c];
-          gcur[c] = gres + tcnt[j];
+          gcur[c] = gres + tcnt;
           // (vxs_partition_exchange: segment c/2 goes straight to its owner's
           // receive buffer at this rank's offset there -- the fused exchange)
           W* base = dst_buf;
@@ -1574,11 +1656,12 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
             const int sg = c >> 1;
             base = reinterpret_cast<W*>(P.xdst[sg]) + P.xoff[sg] - P.childbase[2 * sg];
           }
-          gptr[c] = base + ((long long)gres - (long long)ex);
+          gptr[hslot(c)] = base + ((long long)gres - (long long)ex);
         }
-        ex += tcnt[j];
       }
     }
+    // (this barrier also orders every key read from the stage -- the keys
+    // are in registers by now -- before the staging writes)
     __syncthreads();  // slot counters and gptr ready
     // stage the tile grouped by child: each key takes the next slot of its
     // child (returning shared atomic); the tile's own TMA stage is reused
@@ -1596,7 +1679,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       if (__all_sync(0xffffffffu, same && bk[0] == b0)) {
         // the warp's whole sub-tile is one child: one atomic for 32*ITEMS keys
         unsigned base = 0;
-        if (lane == 0) base = atomicAdd(&whist[hslot(b0)], 32u * ITEMS);
+        if (lane == 0) base = atomicAdd(&whist[b0], 32u * ITEMS);
         base = __shfl_sync(0xffffffffu, base, 0) + lane * ITEMS;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) put(base + i, i);
@@ -1609,30 +1692,31 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
           const int ci = __shfl_sync(0xffffffffu, bk[i], 0);
           if (__all_sync(0xffffffffu, bk[i] == ci)) {
             unsigned base = 0;
-            if (lane == 0) base = atomicAdd(&whist[hslot(ci)], 32u);
+            if (lane == 0) base = atomicAdd(&whist[ci], 32u);
             put(__shfl_sync(0xffffffffu, base, 0) + lane, i);
           } else {
-            put(atomicAdd(&whist[hslot(bk[i])], 1u), i);
+            put(atomicAdd(&whist[bk[i]], 1u), i);
           }
         }
       } else if (cnt == TILE) {  // full tile: every id is valid (straight-line code)
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) put(atomicAdd(&whist[hslot(bk[i])], 1u), i);
+        for (int i = 0; i < ITEMS; ++i) put(atomicAdd(&whist[bk[i]], 1u), i);
       } else {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i)
-          if (bk[i] >= 0) put(atomicAdd(&whist[hslot(bk[i])], 1u), i);
+          if (bk[i] >= 0) put(atomicAdd(&whist[bk[i]], 1u), i);
       }
     }
     W* staged = reinterpret_cast<W*>(stage);
     __syncthreads();
 #ifdef VXS_CHECKS
     // every staged slot j of child c lands inside child c's range
-    auto chk = [&](int c, int j) {
-      VXS_DCHECK(c >= 0 && c < nc, "k_scatter: child id out of range");
+    auto chk = [&](int slot, int j) {
+      const int c = unslot(slot);
+      VXS_DCHECK(slot >= 0 && c < nc, "k_scatter: child id out of range");
       const W* base = dst_buf;  // (exchange: the segment's place in its owner's window)
       if (P.xchg) base = reinterpret_cast<const W*>(P.xdst[c >> 1]) + P.xoff[c >> 1] - P.childbase[2 * (c >> 1)];
-      const long long idx = (long long)((gptr[c] + j) - base);
+      const long long idx = (long long)((gptr[slot] + j) - base);
       const unsigned long long b0 = P.childbase[(unsigned long long)p * kChildStride + c];
       const unsigned long long n0 = P.counts[(unsigned long long)p * kChildStride + c];
       VXS_DCHECK(idx >= (long long)b0 && (unsigned long long)idx < b0 + n0, "k_scatter: key stored outside its child");
@@ -1646,8 +1730,8 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       for (int i = 0; i < ITEMS; ++i) {
         const int j = i * THREADS + threadIdx.x;
         const W v = staged[j];
-        chk(R.child(v), j);
-        gptr[R.child(v)][j] = v;
+        chk(R.slot(v), j);
+        gptr[R.slot(v)][j] = v;
       }
     } else if (out_xf == XF_NONE && cnt == TILE) {
 #pragma unroll
@@ -1661,13 +1745,13 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       if (out_xf == XF_NONE) {
         for (int j = threadIdx.x; j < cnt; j += THREADS) {
           const W v = staged[j];
-          chk(R.child(v), j);
-          gptr[R.child(v)][j] = v;
+          chk(R.slot(v), j);
+          gptr[R.slot(v)][j] = v;
         }
       } else {
         for (int j = threadIdx.x; j < cnt; j += THREADS) {
           const W v = staged[j];
-          gptr[R.child(v)][j] = dec<W>(v, out_xf);
+          gptr[R.slot(v)][j] = dec<W>(v, out_xf);
         }
       }
     } else if (out_xf == XF_NONE) {

@@ -9,6 +9,7 @@
 // read straight from global memory by the consumer.
 #pragma once
 #include <cstdint>
+#include <cstring>
 
 #include "keys.cuh"
 
@@ -134,5 +135,39 @@ __device__ __forceinline__ unsigned char* tile_fixup(const W* g, int cnt, const 
   for (long long j = tl + threadIdx.x; j < cnt; j += THREADS) sts_key<W>(k0, (int)j, ldcs(g + j));
   return k0;
 }
+
+// Full-tile key access in 16-byte chunks (LDS.128): the tile's aligned middle
+// [a0, a1) is nch chunks of KPC keys, thread t owning chunks q*THREADS + t
+// (consecutive threads read consecutive 16 bytes: conflict-free).  A tile
+// that starts off a 16-byte boundary has one chunk fewer; its head and tail
+// keys (KPC in all) fill the last chunk slot of the last thread.  Item i of
+// a thread is key e = i % KPC of its chunk slot q = i / KPC.  Word types of
+// <= 8 bytes only (a 16-byte key need not be 16-byte aligned).
+template <typename W, int THREADS>
+struct TileVec {
+  static constexpr int KPC = 16 / (int)sizeof(W);
+  const unsigned char* kp;  // key 0 of the tile in smem
+  const uint4* mid;         // first aligned chunk = keys [h, h + nch*KPC)
+  int h, nch;
+  __device__ __forceinline__ TileVec(const W* g, const TileSpan& s, const unsigned char* stage,
+                                     const unsigned char* key0)
+      : kp(key0), mid(reinterpret_cast<const uint4*>(stage + (s.a0 - s.base))),
+        h((int)((s.a0 - reinterpret_cast<unsigned long long>(g)) / sizeof(W))), nch((int)((s.a1 - s.a0) >> 4)) {}
+  // tile-relative key index of item i of this thread
+  __device__ __forceinline__ int index(int i) const {
+    const int c = (i / KPC) * THREADS + (int)threadIdx.x, e = i % KPC;
+    return c < nch ? h + c * KPC + e : (e < h ? e : nch * KPC + e);
+  }
+  __device__ __forceinline__ void load(int q, W (&out)[KPC]) const {
+    const int c = q * THREADS + (int)threadIdx.x;
+    if (c < nch) {
+      const uint4 v = mid[c];
+      memcpy(out, &v, 16);
+    } else {
+#pragma unroll
+      for (int e = 0; e < KPC; ++e) out[e] = reinterpret_cast<const W*>(kp)[e < h ? e : nch * KPC + e];
+    }
+  }
+};
 
 }  // namespace vxs

@@ -1607,7 +1607,7 @@ vxs_status vxs_partition(const void* d_keys, size_t n, vxs_key_type type, vxs_or
       fn<<<P.grid, Cfg<W>::kHistThreads, hist_smem<W>(), st>>>(P);
     }
     k_segscan_root<W><<<(kChildStride + 31) / 32, 1024, 0, st>>>(P);
-    k_plan<W><<<1, kChildStride, 0, st>>>(P);
+    k_plan<W><<<grid_for((const void*)k_plan<W>, kChildStride, 0), kChildStride, 0, st>>>(P);  // (+ the tile prefixes)
     {
       auto fn = k_scatter<W>;
       fn<<<P.grid, Cfg<W>::kScatThreads, scatter_smem<W>(), st>>>(P);
@@ -1648,7 +1648,7 @@ vxs_status vxs_partition_counts(const void* d_keys, size_t n, vxs_key_type type,
     k_part_setup<W><<<1, 256, 0, st>>>(P, static_cast<const W*>(d_splitters), nspl, L);
     k_hist<W><<<P.grid, Cfg<W>::kHistThreads, hist_smem<W>(), st>>>(P);
     k_segscan_root<W><<<(kChildStride + 31) / 32, 1024, 0, st>>>(P);
-    k_plan<W><<<1, kChildStride, 0, st>>>(P);
+    k_plan<W><<<grid_for((const void*)k_plan<W>, kChildStride, 0), kChildStride, 0, st>>>(P);  // (+ the tile prefixes)
     k_part_counts<W><<<1, 256, 0, st>>>(P, nseg, reinterpret_cast<unsigned long long*>(d_seg_counts));
     VXS_CK(cudaGetLastError(), "partition_counts");
     return VXS_OK;
