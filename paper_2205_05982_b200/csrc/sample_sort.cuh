@@ -92,7 +92,11 @@ struct Cfg<unsigned long long> {
   static constexpr int kHistCopies = 1;
   static constexpr int kScatMinBlocks = 2;
   static constexpr int kHistMinBlocks = 2;
+#ifdef VXS_U64_HIST3
+  static constexpr int kHistStages = 3;
+#else
   static constexpr int kHistStages = 2;  // (3 would cost an SM's second CTA)
+#endif
   static constexpr int kCap = 8192;
 };
 template <>
@@ -981,7 +985,13 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
   constexpr int ITEMS = TILE / THREADS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ SplSmem<W> S;
-  __shared__ unsigned hist[kChildStride + 1];  // + dump slot
+  // two histograms, alternating by tile: tile t's counts are flushed (read and
+  // zeroed) while tile t+1 is already being counted into the other one, so a
+  // full tile costs one barrier
+  // (<= 4-byte keys; measured slower for 8-byte keys, which keep one
+  // histogram and the barrier after the tile wait)
+  constexpr bool kDbl = sizeof(W) <= 4;
+  __shared__ unsigned hist2[kDbl ? 2 : 1][kChildStride + 1];  // + dump slot
   __shared__ __align__(8) unsigned long long bars[Cfg<W>::kHistStages];
   __shared__ int s_p;
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
@@ -1006,7 +1016,7 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
                  smem_raw + s * stage_bytes<W>(), &bars[s]);
     }
   }
-  for (int i = threadIdx.x; i < kChildStride + 1; i += THREADS) hist[i] = 0;
+  for (int i = threadIdx.x; i < (kDbl ? 2 : 1) * (kChildStride + 1); i += THREADS) (&hist2[0][0])[i] = 0;
   __syncthreads();
   int p = s_p;
   SplitDesc d = list[p];
@@ -1055,13 +1065,16 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
     unsigned char* stage = smem_raw + st * stage_bytes<W>();
     mbar_wait(&bars[st], (phase >> st) & 1);
     phase ^= 1u << st;
-    const unsigned char* kp = tile_fixup<W, THREADS>(src + lo, cnt, span, stage);
-    __syncthreads();
+    unsigned* hist = hist2[kDbl ? (t - t0) & 1 : 0];
+    // full tiles of <= 8-byte keys are read in 16-byte chunks (TileVec layout:
+    // no head / tail fix-up in smem, so no barrier here)
+    constexpr bool kVec = sizeof(W) <= 8;
+    const unsigned char* kp = stage + (reinterpret_cast<unsigned long long>(src + lo) - span.base);
+    if (!(kVec && cnt == TILE)) tile_fixup<W, THREADS>(src + lo, cnt, span, stage);
+    if (!(kDbl && cnt == TILE)) __syncthreads();  // (block-uniform)
     unsigned wide = 0;  // items whose cell holds > 2 splitters (rare)
     const Xf<W> X = make_xf<W>(xf);
-    // full tiles of <= 8-byte keys are read in 16-byte chunks (TileVec layout)
-    constexpr bool kVec = sizeof(W) <= 8;
-    const TileVec<W, THREADS> tv(src + lo, span, stage, kp);
+    const TileVec<W, THREADS> tv(src + lo, span, stage);
     auto count_tile = [&](auto tree_tag, auto flt_tag) {
       constexpr int TREE = decltype(tree_tag)::value;
       constexpr bool FLT = decltype(flt_tag)::value;
@@ -1071,7 +1084,7 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
 #pragma unroll
           for (int q = 0; q < ITEMS / KPC; ++q) {
             W kk[KPC];
-            tv.load(q, kk);
+            tv.load(q, kk, q == ITEMS / KPC - 1);
 #pragma unroll
             for (int e = 0; e < KPC; ++e)
               atomicAdd(&hist[hslot(classify_mode<TREE>(enc_x<FLT>(kk[e], X), S))], 1u);
@@ -1088,9 +1101,23 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
 #pragma unroll
           for (int q = 0; q < ITEMS / KPC; ++q) {
             W kk[KPC];
-            tv.load(q, kk);
+            if constexpr (TREE == 1) {
+              // (tree mode, measured: a global-load path inside this loop
+              // costs low-entropy inputs 15%.  The last thread of a tile off
+              // the 16-byte grid leaves its last chunk slot empty and counts
+              // the tile's KPC head / tail keys from global memory instead.)
+              const bool ok = tv.load_mid(q, kk, q == ITEMS / KPC - 1);
 #pragma unroll
-            for (int e = 0; e < KPC; ++e) bk[q * KPC + e] = classify_mode<TREE>(enc_x<FLT>(kk[e], X), S);
+              for (int e = 0; e < KPC; ++e) bk[q * KPC + e] = ok ? classify_mode<TREE>(enc_x<FLT>(kk[e], X), S) : -2;
+              if (!ok) {
+                for (int e = 0; e < KPC; ++e)
+                  atomicAdd(&hist[hslot(classify(enc_x<FLT>(ldg(src + lo + tv.extra_index(e)), X), S))], 1u);
+              }
+            } else {
+              tv.load(q, kk, q == ITEMS / KPC - 1);
+#pragma unroll
+              for (int e = 0; e < KPC; ++e) bk[q * KPC + e] = classify_mode<TREE>(enc_x<FLT>(kk[e], X), S);
+            }
           }
         } else {
 #pragma unroll
@@ -1107,9 +1134,9 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
           if ((threadIdx.x & 31) == 0) atomicAdd(&hist[hslot(b0)], 32u * ITEMS);
         } else {
 #pragma unroll
-          for (int i = 0; i < ITEMS; ++i) {  // (wide cells count into a dump slot)
+          for (int i = 0; i < ITEMS; ++i) {  // (wide cells and empty slots count into a dump slot)
             atomicAdd(&hist[bk[i] >= 0 ? hslot(bk[i]) : kChildStride], 1u);
-            wide |= (bk[i] < 0 ? 1u : 0u) << i;
+            wide |= (bk[i] == -1 ? 1u : 0u) << i;
           }
         }
       } else {
@@ -1143,8 +1170,8 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
     while (wide) {
       const int i = __ffs(wide) - 1;
       wide &= wide - 1;
-      const int b =
-          classify_slow(enc<W>(lds_key<W>(kp, (kVec && cnt == TILE) ? tv.index(i) : i * THREADS + threadIdx.x), xf), S);
+      const W kx = (kVec && cnt == TILE) ? ldg(src + lo + tv.index(i)) : lds_key<W>(kp, i * THREADS + threadIdx.x);
+      const int b = classify_slow(enc<W>(kx, xf), S);
       VXS_DCHECK(b >= 0 && b < num_children(L), "k_hist: child id out of range");
       atomicAdd(&hist[hslot(b)], 1u);  // rare
     }
@@ -1483,7 +1510,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   unsigned short* stage_b = reinterpret_cast<unsigned short*>(smem_raw + kStages * stage_bytes<W>());
   unsigned* whist = reinterpret_cast<unsigned*>(stage_b + TILE);  // [kChildStride] per-child slot counters
   __shared__ SplSmem<W> S;
-  __shared__ W* gptr[kChildStride];  // where staged slot 0 of child c goes (slot j -> gptr[c][j])
+  __shared__ W* gptr[kChildStride];  // where staged slot 0 of the child in histogram slot s goes (slot j -> gptr[s][j])
   __shared__ unsigned long long gcur[kChildStride];  // this CTA's next global slot per child
   __shared__ __align__(8) unsigned long long bars[kStages];
   __shared__ int s_p;
@@ -1516,7 +1543,11 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     const unsigned long long* sg = P.seg + (unsigned long long)(p + blockIdx.x) * kChildStride;
     const unsigned long long* cb = P.childbase + (unsigned long long)p * kChildStride;
     const int ncl = num_children(L);
-    for (int c = threadIdx.x; c < ncl; c += THREADS) gcur[c] = cb[c] + sg[c];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {  // (thread tid owns children tid*PER + j, here and in the tile loop)
+      const int c = threadIdx.x * PER + j;
+      if (c < ncl) gcur[c] = cb[c] + sg[c];
+    }
   };
   load_cursors();
   const int lane = threadIdx.x & 31;
@@ -1561,8 +1592,13 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     unsigned char* stage = smem_raw + st * stage_bytes<W>();
     mbar_wait(&bars[st], (phase >> st) & 1);
     phase ^= 1u << st;
-    const unsigned char* kp = tile_fixup<W, THREADS>(src + lo, cnt, span, stage);
-    __syncthreads();  // tile complete in smem
+    // (full tiles of <= 8-byte keys: TileVec reads the aligned chunks from
+    // smem and the head / tail keys from global -- no fix-up, no barrier)
+    const unsigned char* kp = stage + (reinterpret_cast<unsigned long long>(src + lo) - span.base);
+    if (!(sizeof(W) <= 8 && cnt == TILE)) {  // (block-uniform)
+      tile_fixup<W, THREADS>(src + lo, cnt, span, stage);
+      __syncthreads();  // tile complete in smem
+    }
     W k[ITEMS];
     int bk[ITEMS];
     unsigned wide = 0;
@@ -1583,11 +1619,11 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       if (cnt == TILE) {  // full tile: no per-key bounds (branch-free classify)
         if constexpr (sizeof(W) <= 8) {  // 16-byte key loads (TileVec layout; any key -> item map works)
           constexpr int KPC = TileVec<W, THREADS>::KPC;
-          const TileVec<W, THREADS> tv(src + lo, span, stage, kp);
+          const TileVec<W, THREADS> tv(src + lo, span, stage);
 #pragma unroll
           for (int q = 0; q < ITEMS / KPC; ++q) {
             W kk[KPC];
-            tv.load(q, kk);
+            tv.load(q, kk, q == ITEMS / KPC - 1);
 #pragma unroll
             for (int e = 0; e < KPC; ++e) {
               const int i = q * KPC + e;
@@ -1663,6 +1699,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     // (this barrier also orders every key read from the stage -- the keys
     // are in registers by now -- before the staging writes)
     __syncthreads();  // slot counters and gptr ready
+
     // stage the tile grouped by child: each key takes the next slot of its
     // child (returning shared atomic); the tile's own TMA stage is reused
     {
@@ -1765,7 +1802,7 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
         gptr[stage_b[j]][j] = dec<W>(staged[j], out_xf);
       }
     }
-    __syncthreads();
+    __syncthreads();  // (measured: deferring the next tile's TMA issue to drop this barrier does not pay)
   }
   if (P.xchg) __threadfence_system();  // peer stores visible before the exchange's barrier
 }

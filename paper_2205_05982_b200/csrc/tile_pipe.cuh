@@ -146,26 +146,43 @@ __device__ __forceinline__ unsigned char* tile_fixup(const W* g, int cnt, const 
 template <typename W, int THREADS>
 struct TileVec {
   static constexpr int KPC = 16 / (int)sizeof(W);
-  const unsigned char* kp;  // key 0 of the tile in smem
-  const uint4* mid;         // first aligned chunk = keys [h, h + nch*KPC)
+  const W* g;        // key 0 of the tile in global memory (head / tail keys are read from there,
+                     // so a full tile needs no tile_fixup and no barrier after the mbarrier wait)
+  const uint4* mid;  // first aligned chunk = keys [h, h + nch*KPC)
   int h, nch;
-  __device__ __forceinline__ TileVec(const W* g, const TileSpan& s, const unsigned char* stage,
-                                     const unsigned char* key0)
-      : kp(key0), mid(reinterpret_cast<const uint4*>(stage + (s.a0 - s.base))),
-        h((int)((s.a0 - reinterpret_cast<unsigned long long>(g)) / sizeof(W))), nch((int)((s.a1 - s.a0) >> 4)) {}
+  __device__ __forceinline__ TileVec(const W* g_, const TileSpan& s, const unsigned char* stage)
+      : g(g_), mid(reinterpret_cast<const uint4*>(stage + (s.a0 - s.base))),
+        h((int)((s.a0 - reinterpret_cast<unsigned long long>(g_)) / sizeof(W))), nch((int)((s.a1 - s.a0) >> 4)) {}
   // tile-relative key index of item i of this thread
   __device__ __forceinline__ int index(int i) const {
     const int c = (i / KPC) * THREADS + (int)threadIdx.x, e = i % KPC;
     return c < nch ? h + c * KPC + e : (e < h ? e : nch * KPC + e);
   }
-  __device__ __forceinline__ void load(int q, W (&out)[KPC]) const {
+  // Chunk slot q from the aligned middle only (false, out[] untouched, when
+  // the slot falls past it -- only a thread's LAST slot can; `last` is a
+  // compile-time value so the other slots carry no test).  The caller handles
+  // the KPC head / tail keys of an unaligned tile itself (extra_index).
+  __device__ __forceinline__ bool load_mid(int q, W (&out)[KPC], bool last) const {
     const int c = q * THREADS + (int)threadIdx.x;
-    if (c < nch) {
+    if (last && c >= nch) return false;
+    const uint4 v = mid[c];
+    memcpy(out, &v, 16);
+    return true;
+  }
+  __device__ __forceinline__ bool unaligned() const { return h != 0; }
+  // tile-relative index of head / tail key e (e < KPC) of an unaligned tile
+  __device__ __forceinline__ int extra_index(int e) const { return e < h ? e : nch * KPC + e; }
+  // `last`: q is the thread's last chunk slot -- the only one that can fall
+  // past the aligned middle (pass a compile-time value: the other slots then
+  // carry no test and no global-load path)
+  __device__ __forceinline__ void load(int q, W (&out)[KPC], bool last) const {
+    const int c = q * THREADS + (int)threadIdx.x;
+    if (!last || c < nch) {
       const uint4 v = mid[c];
       memcpy(out, &v, 16);
     } else {
 #pragma unroll
-      for (int e = 0; e < KPC; ++e) out[e] = reinterpret_cast<const W*>(kp)[e < h ? e : nch * KPC + e];
+      for (int e = 0; e < KPC; ++e) out[e] = ldcs(g + (e < h ? e : nch * KPC + e));
     }
   }
 };
