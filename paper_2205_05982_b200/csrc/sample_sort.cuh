@@ -636,16 +636,10 @@ struct RadixReg {
   int shift;
   unsigned m;
   unsigned mul;
-  unsigned cmax;
-  int lshift;
-  const unsigned* t1;
-  bool pw;  // piecewise radix (mode 4; block-uniform)
   __device__ __forceinline__ explicit RadixReg(const SplSmem<W>& S)
-      : lo(S.lo), shift(S.shift), m((unsigned)S.m), mul(S.mul), cmax(S.cmax), lshift(S.lshift), t1(S.t1),
-        pw(S.use_tree == 4) {}
+      : lo(S.lo), shift(S.shift), m((unsigned)S.m), mul(S.mul) {}
   // shared-histogram slot of x's child (= its digit: radix children are even, hslot(2d) = d)
   __device__ __forceinline__ int slot(const W& x) const {
-    if (pw) return (int)pw_digit(x, lo, shift, lshift, cmax, t1);
     if constexpr (sizeof(W) == 8) return (int)radix_digit_hi(x, lo, shift, mul, m);  // (mode 3 only)
     else return (int)radix_digit(x, lo, shift, mul, m);
   }
@@ -1604,9 +1598,9 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     unsigned wide = 0;
     const Xf<W> X = make_xf<W>(xf);
     // recompute child ids at write-out instead of staging them (cheap for
-    // <= 32-bit words, the 64-bit high-word classifier and piecewise radix)
-    const bool radix =
-        (sizeof(W) <= 4 && S.use_tree == 2) || (sizeof(W) == 8 && S.use_tree == 3) || S.use_tree == 4;
+    // <= 32-bit words and the 64-bit high-word classifier; piecewise radix
+    // stages them: f32 1e8 scatter@L0 0.39 -> 0.34 ms)
+    const bool radix = (sizeof(W) <= 4 && S.use_tree == 2) || (sizeof(W) == 8 && S.use_tree == 3);
     // bk[] holds each key's shared-histogram SLOT (hslot of its child id; the
     // digit itself in the radix modes), or -1 (wide cell) / -2 (past the tile)
     auto classify_tile = [&](auto tree_tag, auto flt_tag) {
@@ -1709,18 +1703,24 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
         staged[pos] = k[i];
         if (!radix) stage_b[pos] = (unsigned short)bk[i];
       };
-      bool same = bk[0] >= 0;
-#pragma unroll
-      for (int i = 1; i < ITEMS; ++i) same = same && bk[i] == bk[0];
+      // (random keys leave here at once: the first and last lane's first
+      // keys already differ, and neither fast path below can apply)
       const int b0 = __shfl_sync(0xffffffffu, bk[0], 0);
-      if (__all_sync(0xffffffffu, same && bk[0] == b0)) {
+      const bool ends = __shfl_sync(0xffffffffu, bk[0], 31) == b0;  // (warp-uniform)
+      bool same = false;
+      if (ends) {
+        same = bk[0] >= 0;
+#pragma unroll
+        for (int i = 1; i < ITEMS; ++i) same = same && bk[i] == bk[0];
+      }
+      if (ends && __all_sync(0xffffffffu, same && bk[0] == b0)) {
         // the warp's whole sub-tile is one child: one atomic for 32*ITEMS keys
         unsigned base = 0;
         if (lane == 0) base = atomicAdd(&whist[b0], 32u * ITEMS);
         base = __shfl_sync(0xffffffffu, base, 0) + lane * ITEMS;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) put(base + i, i);
-      } else if (cnt == TILE && __shfl_sync(0xffffffffu, bk[0], 31) == b0) {
+      } else if (cnt == TILE && ends) {
         // presorted-looking warp (its first 32-key slice is one child): slice
         // by slice, one atomic per uniform slice -- 32 lanes would otherwise
         // serialise on the same counter

@@ -1,11 +1,10 @@
 L=paper_2205_05982_b200/lib
 cp $L/libvxsort_b200.so /tmp/keep.so
-python -m pytest tests/test_sort_gpu.py tests/test_dist_ops_gpu.py -m gpu -x -q 2>&1 | tail -2
 for r in 1; do
-  for v in A B C; do
+  for v in ${VARIANTS:-A B C}; do
     cp $L/lib$v.so $L/libvxsort_b200.so
-    for w in c2-u32-asc u64-uniform c3a c3f c2-f32-asc; do
-      echo -n "$v "; timeout 120 python tools/time_kernels.py --workload $w --reps 5 | cut -c1-330
+    for w in ${WL:-c2-u32-asc u64-uniform c3a c3f c2-f32-asc}; do
+      echo -n "$v "; timeout 120 python tools/time_kernels.py --workload $w --reps 5 | cut -c1-${CUT:-330}
     done
   done
 done
