@@ -52,9 +52,17 @@ struct SplitDesc {
   unsigned long long start, size, tile_base;
   unsigned long long aux;  // radix mode: digit multiplier M (digit = f * M >> 32)
   unsigned flags, L;       // L: bits 0-7 fan-out exponent, bit 8 radix mode, bit 9 piecewise
-                           //    radix over the splitters, bits 16-23 shift, bits 24-31 distinct
-                           //    splitter count when < 2^L - 1
+                           //    radix over the splitters, bits 10-11 tile cost weight - 1,
+                           //    bits 16-23 shift, bits 24-31 distinct splitter count when < 2^L - 1
+  // Cost-weighted tile order of the level (k_sample's last CTA, level_ranges):
+  // the bucket's tiles start at virtual position vbase and are `weight` units
+  // long each; CTA b of k_hist / k_scatter owns the tiles that start inside
+  // [b * vpc, (b + 1) * vpc).  bfirst / blast: first / last CTA with a tile of
+  // this bucket (rows p + bfirst .. p + blast of the offset table).
+  unsigned long long vbase;
+  unsigned bfirst, blast;
 };
+__host__ __device__ __forceinline__ unsigned tile_weight(unsigned L) { return ((L >> 10) & 3u) + 1u; }
 
 struct Item {
   unsigned long long start, size;
@@ -66,7 +74,8 @@ struct Ctrl {
   unsigned long long split_packed[2];  // (count << 40) | tiles, per split list
   unsigned long long item_count[kNumLists];
   unsigned long long partition_calls, keys_partitioned, base_cases;
-  unsigned error, pad;
+  unsigned error;
+  unsigned sample_done;  // k_sample CTAs finished (the last one lays out the level's CTA tile ranges)
   unsigned modes[8][4];  // (diagnostics) buckets per level: splitter table/tree, radix, piecewise radix
 };
 
@@ -188,6 +197,7 @@ struct Params {
   unsigned long long* childbase;  // [cap_split][kChildStride] absolute start of each child
   unsigned short* tilecnt;      // [tiles][kChildStride] per-tile child counts (k_hist -> k_scatter)
   int grid;                     // CTAs of k_hist and k_scatter (identical tile ranges)
+  unsigned long long* cta_t0;   // [grid + 1] first tile of every CTA this level (level_ranges)
   int root_init;                // k_sample sets up the root bucket (level-0 launch; see k_sample)
   Item* items[kNumLists];
   unsigned long long cap_split, cap_items;
@@ -678,6 +688,78 @@ __device__ __forceinline__ int find_bucket(const SplitDesc* list, int nb, unsign
   return lo;
 }
 
+// Cost-weighted CTA tile ranges of one level (run by ONE CTA after every
+// bucket's classifier is known).  A tile of a radix bucket costs 1 unit, a
+// tile of a splitter-table / tree / piecewise bucket 2 (measured ~2x per key
+// in k_hist): with equal tile counts per CTA the CTAs inside such buckets set
+// the pace of the whole level (normal floats: 4% of the level-1 buckets made
+// k_hist 2x and k_scatter 1.4x slower).  Ranges stay contiguous and ordered,
+// so the (bucket p, CTA b) offset rows p + b are still unique along the tile
+// order.  Writes SplitDesc::vbase / bfirst / blast and P.cta_t0[0 .. grid].
+template <typename W>
+__device__ __forceinline__ void level_ranges(const Params<W>& P, SplitDesc* list, int nb, unsigned long long T) {
+  __shared__ unsigned long long lr_scan[32];
+  __shared__ unsigned long long lr_carry;
+  const int THREADS = (int)blockDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = THREADS >> 5;
+  if (threadIdx.x == 0) lr_carry = 0;
+  __syncthreads();
+  for (int p0 = 0; p0 < nb; p0 += THREADS) {  // exclusive scan of ntiles * weight over the buckets
+    const int q = p0 + (int)threadIdx.x;
+    unsigned long long v = 0;
+    if (q < nb) v = (unsigned long long)ntiles_dev<W>(__ldcg(&list[q].size)) * tile_weight(__ldcg(&list[q].L));
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) lr_scan[warp] = x;
+    __syncthreads();
+    unsigned long long before = lr_carry, all = 0;
+    for (int w2 = 0; w2 < nw; ++w2) {
+      before += w2 < warp ? lr_scan[w2] : 0ull;
+      all += lr_scan[w2];
+    }
+    if (q < nb) list[q].vbase = before + x - v;
+    __syncthreads();
+    if (threadIdx.x == 0) lr_carry += all;
+    __syncthreads();
+  }
+  const unsigned long long V = lr_carry;
+  const unsigned long long G = (unsigned long long)P.grid;
+  // vpc >= the largest weight: every CTA between a bucket's first and last
+  // then owns at least one of its tiles (k_plan / k_segscan_root read the
+  // offset rows of ALL those CTAs)
+  unsigned long long vpc = (V + G - 1) / G;
+  if (vpc < 4) vpc = 4;
+  for (int q = threadIdx.x; q < nb; q += THREADS) {
+    const unsigned long long vb = list[q].vbase;
+    const unsigned long long nt = (unsigned long long)ntiles_dev<W>(__ldcg(&list[q].size));
+    list[q].bfirst = (unsigned)(vb / vpc);
+    list[q].blast = (unsigned)((vb + (nt - 1) * tile_weight(__ldcg(&list[q].L))) / vpc);
+  }
+  // first tile of CTA b = the first tile whose virtual start is >= b * vpc
+  for (unsigned long long b = threadIdx.x; b <= G; b += THREADS) {
+    const unsigned long long x = b * vpc;
+    unsigned long long t = T;
+    if (nb > 0 && x < V) {
+      int lo = 0, hi = nb - 1;  // last bucket with vbase <= x
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (list[mid].vbase <= x) lo = mid;
+        else hi = mid - 1;
+      }
+      const unsigned long long w = tile_weight(__ldcg(&list[lo].L));
+      const unsigned long long nt = (unsigned long long)ntiles_dev<W>(__ldcg(&list[lo].size));
+      const unsigned long long i = (x - list[lo].vbase + w - 1) / w;
+      const unsigned long long tb = __ldcg(&list[lo].tile_base);
+      t = i < nt ? tb + i : tb + nt;  // (tb + nt: the next bucket's first tile, or T)
+    }
+    P.cta_t0[b] = t;
+  }
+}
+
 // ---- kernels ---------------------------------------------------------------
 
 // Root setup: reset counters; the whole array becomes one split bucket or one
@@ -690,6 +772,7 @@ __device__ __forceinline__ void init_root(const Params<W>& P) {
   for (int i = 0; i < kNumLists; ++i) c->item_count[i] = 0;
   c->partition_calls = c->keys_partitioned = c->base_cases = 0;
   c->error = 0;
+  c->sample_done = 0;
   for (int i = 0; i < 32; ++i) c->modes[i / 4][i % 4] = 0;
   if (P.n > (unsigned long long)Cfg<W>::kCap || P.part_mode) {
     SplitDesc d;
@@ -699,6 +782,8 @@ __device__ __forceinline__ void init_root(const Params<W>& P) {
     d.flags = F_RAW;
     d.L = 0;
     d.aux = 0;
+    d.vbase = 0;
+    d.bfirst = d.blast = 0;
     P.split[0][0] = d;
     c->split_packed[0] = (1ull << 40) | (unsigned long long)ntiles_dev<W>(P.n);
   } else if (P.n > 1) {
@@ -909,13 +994,28 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
       }
     }
     if (threadIdx.x == 0) {
-      list[p].L = (unsigned)Lf | (radix ? (0x100u | ((unsigned)dshift << 16)) : 0u) | (pw ? 0x200u : 0u) |
+      // (tile cost weight 2 for every classifier but the plain radix digit: level_ranges)
+      list[p].L = (unsigned)Lf | (radix ? (0x100u | ((unsigned)dshift << 16)) : 0x400u) | (pw ? 0x200u : 0u) |
                   (meff << 24);
       list[p].aux = dmul;
       atomicAdd(&P.ctrl->modes[P.level < 8 ? P.level : 7][radix ? 1 : (pw ? 2 : 0)], 1u);
     }
     __syncthreads();
   }
+  // the last CTA to finish lays out the level's cost-weighted CTA tile ranges
+  __shared__ unsigned s_ticket;
+  bool last = P.root_init != 0;  // (root level: CTA 0 is the only one here)
+  if (!last) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_ticket = atomicAdd(&P.ctrl->sample_done, 1u);
+    __syncthreads();
+    last = s_ticket == gridDim.x - 1;
+  }
+  if (!last) return;
+  if (threadIdx.x == 0) P.ctrl->sample_done = 0;
+  __threadfence();
+  level_ranges(P, list, nb, P.root_init ? (unsigned long long)ntiles_dev<W>(P.n) : (packed & kTileMask));
 }
 
 // Tile t of the current level: owning bucket, first key and key count.
@@ -990,11 +1090,9 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
   __shared__ int s_p;
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
   const int nb = (int)(packed >> 40);
-  const unsigned long long T = packed & kTileMask;
   if (nb == 0) return;
-  const unsigned long long tpc = (T + gridDim.x - 1) / gridDim.x;
-  const unsigned long long t0 = blockIdx.x * tpc;
-  const unsigned long long t1 = t0 + tpc < T ? t0 + tpc : T;
+  const unsigned long long t0 = P.cta_t0[blockIdx.x];  // (cost-weighted ranges: level_ranges)
+  const unsigned long long t1 = P.cta_t0[blockIdx.x + 1];
   if (t0 >= t1) return;
   const SplitDesc* list = P.split[P.cur];
   TileCursor<W> ic;  // (thread 0: the tile issuer)
@@ -1195,64 +1293,21 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
   }
 }
 
-// Column scan of the per-(bucket p, CTA b) child counts written by k_hist:
-// slot (p + b) becomes the offset of CTA b's keys inside child c, and the
-// per-child totals go to counts[p][c].  Work item = (bucket, 32 children);
-// one warp per item, 16 independent loads in flight per lane.
-template <typename W>
-__global__ void __launch_bounds__(128) k_segscan(Params<W> P) {
-  pdl_enter();
-  const unsigned long long packed = P.ctrl->split_packed[P.cur];
-  const int nb = (int)(packed >> 40);
-  const unsigned long long T = packed & kTileMask;
-  if (nb == 0) return;
-  const unsigned long long tpc = (T + P.grid - 1) / P.grid;
-  const SplitDesc* list = P.split[P.cur];
-  constexpr int kChunks = kChildStride / 32;
-  const int lane = threadIdx.x & 31;
-  const long long nwork = (long long)nb * kChunks;
-  for (long long w = (long long)blockIdx.x * 4 + (threadIdx.x >> 5); w < nwork; w += (long long)gridDim.x * 4) {
-    const int p = (int)(w / kChunks);
-    const int c = (int)(w % kChunks) * 32 + lane;
-    const SplitDesc d = list[p];
-    const int nc = num_children((int)(d.L & 0xFFu));
-    if ((int)(w % kChunks) * 32 >= nc) continue;
-    const unsigned long long nt = (unsigned long long)ntiles_dev<W>(d.size);
-    const int b_first = (int)(d.tile_base / tpc);
-    const int b_last = (int)((d.tile_base + nt - 1) / tpc);
-    unsigned long long cnt = 0;
-    if (c < nc) {
-      constexpr int B = 16;
-      for (int b0 = b_first; b0 <= b_last; b0 += B) {
-        unsigned long long v[B];
-#pragma unroll
-        for (int j = 0; j < B; ++j)
-          v[j] = b0 + j <= b_last ? P.seg[(unsigned long long)(p + b0 + j) * kChildStride + c] : 0ull;
-#pragma unroll
-        for (int j = 0; j < B; ++j) {
-          if (b0 + j <= b_last) P.seg[(unsigned long long)(p + b0 + j) * kChildStride + c] = cnt;
-          cnt += v[j];
-        }
-      }
-      P.counts[(unsigned long long)p * kChildStride + c] = cnt;
-    }
-  }
-}
-
-// k_segscan for the root level (one bucket, every CTA of the grid holds a
-// row): one CTA per 32-child chunk, its 32 warps split the rows (one
-// round trip of loads instead of a serial walk down ~300 rows per lane).
+// Column scan of the root level's per-CTA child counts written by k_hist
+// (one bucket, every CTA of the grid holds a row): row b becomes the offset
+// of CTA b's keys inside each child, the per-child totals go to counts[].
+// One CTA per 32-child chunk, its 32 warps split the rows (one round trip of
+// loads instead of a serial walk down ~300 rows per lane).  Deeper levels
+// scan their handful of rows per bucket in k_plan.
 template <typename W>
 __global__ void __launch_bounds__(1024) k_segscan_root(Params<W> P) {
   pdl_enter();
   __shared__ unsigned long long part[32][33];
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
   if ((int)(packed >> 40) == 0) return;
-  const unsigned long long T = packed & kTileMask;
-  const unsigned long long tpc = (T + P.grid - 1) / P.grid;
   const SplitDesc d = P.split[P.cur][0];
   const int nc = num_children((int)(d.L & 0xFFu));
-  const int rows = (int)((ntiles_dev<W>(d.size) + tpc - 1) / tpc);  // CTAs b = 0 .. rows-1
+  const int rows = (int)d.blast + 1;  // CTAs b = 0 .. rows-1 hold tiles
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int per = (rows + 31) / 32;
   constexpr int R = 16;
@@ -1322,10 +1377,7 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
     } else if (c < nc) {
       // column scan of child c over the CTA rows touching this bucket (a
       // handful below the root): row slots become offsets, the sum the total
-      const unsigned long long T = P.ctrl->split_packed[P.cur] & kTileMask;
-      const unsigned long long tpc = (T + P.grid - 1) / P.grid;
-      const int b_first = (int)(d.tile_base / tpc);
-      const int b_last = (int)((d.tile_base + (unsigned long long)ntiles_dev<W>(d.size) - 1) / tpc);
+      const int b_first = (int)d.bfirst, b_last = (int)d.blast;
       for (int b = b_first; b <= b_last; ++b) {
         unsigned long long* sl = P.seg + (unsigned long long)(p + b) * kChildStride + c;
         const unsigned long long v = *sl;
@@ -1366,6 +1418,8 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
         nd.flags = child_flags;
         nd.L = 0;
         nd.aux = 0;
+        nd.vbase = 0;
+        nd.bfirst = nd.blast = 0;
         P.split[nxt][q] = nd;
       } else {
         P.ctrl->error = 1;
@@ -1510,11 +1564,9 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
   __shared__ int s_p;
   const unsigned long long packed = P.ctrl->split_packed[P.cur];
   const int nb = (int)(packed >> 40);
-  const unsigned long long T = packed & kTileMask;
   if (nb == 0) return;
-  const unsigned long long tpc = (T + gridDim.x - 1) / gridDim.x;
-  const unsigned long long t0 = blockIdx.x * tpc;
-  const unsigned long long t1 = t0 + tpc < T ? t0 + tpc : T;
+  const unsigned long long t0 = P.cta_t0[blockIdx.x];  // (cost-weighted ranges: level_ranges)
+  const unsigned long long t1 = P.cta_t0[blockIdx.x + 1];
   if (t0 >= t1) return;
   const SplitDesc* list = P.split[P.cur];
   TileCursor<W> ic;  // (thread 0: the tile issuer)
@@ -2006,6 +2058,8 @@ __global__ void k_part_setup(Params<W> P, const W* spl, int nspl, int L) {
   for (int i = threadIdx.x; i < m; i += blockDim.x) P.splitters[i] = i < nspl ? spl[i] : key_max<W>();
   for (int i = threadIdx.x; i < kChildStride; i += blockDim.x) P.counts[i] = 0;
   if (threadIdx.x == 0) P.split[0][0].L = (unsigned)L;
+  __syncthreads();
+  level_ranges(P, P.split[0], 1, (unsigned long long)ntiles_dev<W>(P.n));
 }
 
 // Per-segment counts: segment i holds children 2i (keys between splitters)

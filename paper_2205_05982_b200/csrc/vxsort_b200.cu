@@ -211,7 +211,7 @@ int stream_grid() {
   return g < kMaxGrid ? g : kMaxGrid;
 }
 struct Layout {
-  size_t tmp, split0, split1, splitters, counts, childbase, seg, tilecnt, items[kNumLists], ctrl, total;
+  size_t tmp, split0, split1, splitters, counts, childbase, seg, tilecnt, cta_t0, items[kNumLists], ctrl, total;
   unsigned long long cap_split, cap_items;
 };
 
@@ -237,6 +237,7 @@ Layout layout_for(size_t n) {
   // per-tile child counts of one level: at most n / Tile full tiles plus one
   // partial tile per split bucket
   L.tilecnt = take((n / Cfg<W>::kTile + L.cap_split + 1) * kChildStride * sizeof(unsigned short));
+  L.cta_t0 = take((kMaxGrid + 1) * sizeof(unsigned long long));
   for (int i = 0; i < kNumLists; ++i) L.items[i] = take(L.cap_items * sizeof(Item));
   L.ctrl = take(sizeof(Ctrl));
   L.total = off;
@@ -263,6 +264,7 @@ Params<W> make_params(W* keys, size_t n, int xf, uint64_t seed, unsigned char* w
   P.childbase = reinterpret_cast<unsigned long long*>(ws + L.childbase);
   P.tilecnt = reinterpret_cast<unsigned short*>(ws + L.tilecnt);
   P.grid = stream_grid<W>();
+  P.cta_t0 = reinterpret_cast<unsigned long long*>(ws + L.cta_t0);
   for (int i = 0; i < kNumLists; ++i) P.items[i] = reinterpret_cast<Item*>(ws + L.items[i]);
   P.cap_split = L.cap_split;
   P.cap_items = L.cap_items;
