@@ -52,7 +52,7 @@ struct SplitDesc {
   unsigned long long start, size, tile_base;
   unsigned long long aux;  // radix mode: digit multiplier M (digit = f * M >> 32)
   unsigned flags, L;       // L: bits 0-7 fan-out exponent, bit 8 radix mode, bit 9 piecewise
-                           //    radix over the splitters, bits 10-11 tile cost weight - 1,
+                           //    radix over the splitters, bit 10 tile cost weight - 1,
                            //    bits 16-23 shift, bits 24-31 distinct splitter count when < 2^L - 1
   // Cost-weighted tile order of the level (k_sample's last CTA, level_ranges):
   // the bucket's tiles start at virtual position vbase and are `weight` units
@@ -62,7 +62,8 @@ struct SplitDesc {
   unsigned long long vbase;
   unsigned bfirst, blast;
 };
-__host__ __device__ __forceinline__ unsigned tile_weight(unsigned L) { return ((L >> 10) & 3u) + 1u; }
+constexpr unsigned kMaxTileWeight = 2;  // (k_sample sets weight 1 or 2)
+__host__ __device__ __forceinline__ unsigned tile_weight(unsigned L) { return ((L >> 10) & 1u) + 1u; }
 
 struct Item {
   unsigned long long start, size;
@@ -700,8 +701,26 @@ template <typename W>
 __device__ __forceinline__ void level_ranges(const Params<W>& P, SplitDesc* list, int nb, unsigned long long T) {
   __shared__ unsigned long long lr_scan[32];
   __shared__ unsigned long long lr_carry;
+  constexpr int kVbCache = 1024;  // vbase of the first buckets cached for the searches below
+  __shared__ unsigned long long lr_vb[kVbCache];
   const int THREADS = (int)blockDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = THREADS >> 5;
+  const unsigned long long G = (unsigned long long)P.grid;
+  if (nb == 1) {  // (root level, vxs_partition: closed form, no scan, no search)
+    const unsigned long long w = tile_weight(__ldcg(&list[0].L));
+    unsigned long long vpc = (T * w + G - 1) / G;
+    if (vpc < w) vpc = w;  // (see below)
+    if (threadIdx.x == 0) {
+      list[0].vbase = 0;
+      list[0].bfirst = 0;
+      list[0].blast = (unsigned)(T ? (T - 1) * w / vpc : 0);
+    }
+    for (unsigned long long b = threadIdx.x; b <= G; b += THREADS) {
+      const unsigned long long i = (b * vpc + w - 1) / w;
+      P.cta_t0[b] = i < T ? i : T;
+    }
+    return;
+  }
   if (threadIdx.x == 0) lr_carry = 0;
   __syncthreads();
   for (int p0 = 0; p0 < nb; p0 += THREADS) {  // exclusive scan of ntiles * weight over the buckets
@@ -721,18 +740,20 @@ __device__ __forceinline__ void level_ranges(const Params<W>& P, SplitDesc* list
       before += w2 < warp ? lr_scan[w2] : 0ull;
       all += lr_scan[w2];
     }
-    if (q < nb) list[q].vbase = before + x - v;
+    if (q < nb) {
+      list[q].vbase = before + x - v;
+      if (q < kVbCache) lr_vb[q] = before + x - v;
+    }
     __syncthreads();
     if (threadIdx.x == 0) lr_carry += all;
     __syncthreads();
   }
   const unsigned long long V = lr_carry;
-  const unsigned long long G = (unsigned long long)P.grid;
   // vpc >= the largest weight: every CTA between a bucket's first and last
   // then owns at least one of its tiles (k_plan / k_segscan_root read the
   // offset rows of ALL those CTAs)
   unsigned long long vpc = (V + G - 1) / G;
-  if (vpc < 4) vpc = 4;
+  if (vpc < kMaxTileWeight) vpc = kMaxTileWeight;
   for (int q = threadIdx.x; q < nb; q += THREADS) {
     const unsigned long long vb = list[q].vbase;
     const unsigned long long nt = (unsigned long long)ntiles_dev<W>(__ldcg(&list[q].size));
@@ -747,12 +768,12 @@ __device__ __forceinline__ void level_ranges(const Params<W>& P, SplitDesc* list
       int lo = 0, hi = nb - 1;  // last bucket with vbase <= x
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (list[mid].vbase <= x) lo = mid;
+        if ((mid < kVbCache ? lr_vb[mid] : list[mid].vbase) <= x) lo = mid;
         else hi = mid - 1;
       }
       const unsigned long long w = tile_weight(__ldcg(&list[lo].L));
       const unsigned long long nt = (unsigned long long)ntiles_dev<W>(__ldcg(&list[lo].size));
-      const unsigned long long i = (x - list[lo].vbase + w - 1) / w;
+      const unsigned long long i = (x - (lo < kVbCache ? lr_vb[lo] : list[lo].vbase) + w - 1) / w;
       const unsigned long long tb = __ldcg(&list[lo].tile_base);
       t = i < nt ? tb + i : tb + nt;  // (tb + nt: the next bucket's first tile, or T)
     }
