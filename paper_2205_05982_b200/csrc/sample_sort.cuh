@@ -52,7 +52,8 @@ struct SplitDesc {
   unsigned long long start, size, tile_base;
   unsigned long long aux;  // radix mode: digit multiplier M (digit = f * M >> 32)
   unsigned flags, L;       // L: bits 0-7 fan-out exponent, bit 8 radix mode, bit 9 piecewise
-                           //    radix over the splitters, bit 10 tile cost weight - 1,
+                           //    radix over the splitters, bit 10 tile cost weight - 1, bit 11 radix over the
+                           //    bucket's known bounds (unclamped digit),
                            //    bits 16-23 shift, bits 24-31 distinct splitter count when < 2^L - 1
   // Cost-weighted tile order of the level (k_sample's last CTA, level_ranges):
   // the bucket's tiles start at virtual position vbase and are `weight` units
@@ -61,8 +62,19 @@ struct SplitDesc {
   // this bucket (rows p + bfirst .. p + blast of the offset table).
   unsigned long long vbase;
   unsigned bfirst, blast;
+  // Bounds every key of the bucket lies within (transformed domain, <= 8-byte
+  // words; the whole word range at the root, a radix parent's digit cell
+  // below it -- k_plan).  A radix split over [klo, khi] needs no per-key
+  // clamps (L bit 11, classify_mode<5/6>).
+  unsigned long long klo, khi;
 };
 constexpr unsigned kMaxTileWeight = 2;  // (k_sample sets weight 1 or 2)
+// Largest word value as u64 (bucket bounds; 16-byte words carry none).
+template <typename W>
+__host__ __device__ __forceinline__ unsigned long long word_max_u64() {
+  if constexpr (sizeof(W) >= 8) return ~0ull;
+  else return (1ull << (8 * sizeof(W))) - 1ull;
+}
 __host__ __device__ __forceinline__ unsigned tile_weight(unsigned L) { return ((L >> 10) & 1u) + 1u; }
 
 struct Item {
@@ -334,6 +346,19 @@ __device__ __forceinline__ unsigned radix_digit(const U128& x, const U128& lo, i
   return umin(__umulhi(key_shr32(key_sub(x, lo), shift), mul), m);
 }
 
+// Digit of x in a bucket whose keys are KNOWN to lie in [lo, hi] (SplitDesc
+// klo / khi) with the multiplier fitted to hi: no clamp below, none above.
+template <typename W>
+__device__ __forceinline__ unsigned radix_digit_unc(const W& x, const W& lo, int shift, unsigned mul) {
+  return __umulhi(key_shr32(key_sub(x, lo), shift), mul);
+}
+// Same on the high words (64-bit keys, shift >= 32; lo has a zero low word,
+// so hi(x) - hi(lo) is exact).
+__device__ __forceinline__ unsigned radix_digit_unc_hi(unsigned long long x, unsigned long long lo, int shift,
+                                                       unsigned mul) {
+  return __umulhi(((unsigned)(x >> 32) - (unsigned)(lo >> 32)) >> (shift - 32), mul);
+}
+
 template <typename W>
 struct SplSmem {
   W srt[257];  // m splitters, padded with the maximum up to 255, + sentinel
@@ -346,7 +371,8 @@ struct SplSmem {
   int lshift;     // table modes: fine unit = min(raw unit, cmax) << lshift (small ranges)
   int tdepth;     // tree mode: levels (2^tdepth - 1 >= m; shallow for few splitters)
   int shift, m, use_tree;  // use_tree: 0 table, 1 tree, 2 radix (equal-width digits),
-                           //   3 radix on the high word (64-bit keys, shift >= 32)
+                           //   3 radix on the high word (64-bit keys, shift >= 32), 4 piecewise
+                           //   radix, 5 / 6 = 2 / 3 over the bucket's known bounds (unclamped)
   unsigned mul;  // radix mode multiplier (radix_digit)
   unsigned short lut[kLut];  // (first, end) splitter index of cell c, packed lo | hi << 8
 };
@@ -506,6 +532,7 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, unsigned lraw, Sp
       S.m = m;
       S.mul = (unsigned)aux;
       S.use_tree = (sizeof(W) == 8 && S.shift >= 32) ? 3 : 2;
+      if (lraw & 0x800u) S.use_tree += 3;  // known bounds: unclamped digit
     }
     __syncthreads();
     return;
@@ -600,7 +627,11 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, unsigned lraw, Sp
 // lands in equality bucket 2m+1).
 template <int MODE, typename W>
 __device__ __forceinline__ int classify_mode(const W& x, const SplSmem<W>& S) {
-  if constexpr (MODE == 4) {
+  if constexpr (MODE == 6 && sizeof(W) == 8) {
+    return 2 * (int)radix_digit_unc_hi(x, S.lo, S.shift, S.mul);
+  } else if constexpr (MODE >= 5) {
+    return 2 * (int)radix_digit_unc(x, S.lo, S.shift, S.mul);
+  } else if constexpr (MODE == 4) {
     return 2 * (int)pw_digit(x, S.lo, S.shift, S.lshift, S.cmax, S.t1);
   } else if constexpr (MODE == 3 && sizeof(W) == 8) {
     return 2 * (int)radix_digit_hi(x, S.lo, S.shift, S.mul, (unsigned)S.m);
@@ -649,16 +680,25 @@ struct RadixReg {
   unsigned mul;
   __device__ __forceinline__ explicit RadixReg(const SplSmem<W>& S)
       : lo(S.lo), shift(S.shift), m((unsigned)S.m), mul(S.mul) {}
-  // shared-histogram slot of x's child (= its digit: radix children are even, hslot(2d) = d)
+  // shared-histogram slot of x's child (= its digit: radix children are even, hslot(2d) = d);
+  // UNC: the bucket's known-bounds digit (modes 5 / 6)
+  template <bool UNC>
   __device__ __forceinline__ int slot(const W& x) const {
-    if constexpr (sizeof(W) == 8) return (int)radix_digit_hi(x, lo, shift, mul, m);  // (mode 3 only)
-    else return (int)radix_digit(x, lo, shift, mul, m);
+    if constexpr (sizeof(W) == 8) {  // (high-word modes 3 / 6 only)
+      if constexpr (UNC) return (int)radix_digit_unc_hi(x, lo, shift, mul);
+      else return (int)radix_digit_hi(x, lo, shift, mul, m);
+    } else {
+      if constexpr (UNC) return (int)radix_digit_unc(x, lo, shift, mul);
+      else return (int)radix_digit(x, lo, shift, mul, m);
+    }
   }
 };
 
 template <typename W>
 __device__ __forceinline__ int classify_fast(const W& x, const SplSmem<W>& S) {
-  return S.use_tree == 4 ? classify_mode<4>(x, S)
+  return S.use_tree == 6 ? classify_mode<6>(x, S)
+         : S.use_tree == 5 ? classify_mode<5>(x, S)
+         : S.use_tree == 4 ? classify_mode<4>(x, S)
          : S.use_tree == 3 ? classify_mode<3>(x, S)
                         : S.use_tree == 2 ? classify_mode<2>(x, S)
                                           : (S.use_tree ? classify_mode<1>(x, S) : classify_mode<0>(x, S));
@@ -781,6 +821,49 @@ __device__ __forceinline__ void level_ranges(const Params<W>& P, SplitDesc* list
   }
 }
 
+// Key bounds of child c of bucket d (SplitDesc::klo / khi of the child).
+// Every child inherits its parent's bounds; an even child 2*dd of a radix
+// split is further confined to its digit's cell: with f = (x - lo) >> sh
+// (or the same on the high words) and digit = f * mul >> 32, digit dd holds
+// exactly the f in [ceil(dd * 2^32 / mul), ceil((dd + 1) * 2^32 / mul)).  A
+// clamped split (digits over the sample range) leaves digit 0 open below and
+// its last digit -- and any digit reached by a saturated f -- open above.
+// Must mirror radix_digit / radix_digit_hi / radix_digit_unc* exactly: the
+// unclamped digit of the NEXT level trusts these bounds.
+template <typename W>
+__device__ __forceinline__ void child_bounds(const SplitDesc& d, unsigned long long lo, int c,
+                                             unsigned long long& klo, unsigned long long& khi) {
+  klo = d.klo;
+  khi = d.khi;
+  if (sizeof(W) > 8 || !(d.L & 0x100u) || (c & 1)) return;
+  const unsigned long long mul = d.aux;
+  if (mul == 0) return;
+  const int sh = (int)((d.L >> 16) & 0xFFu);
+  const unsigned long long dd = (unsigned long long)(c >> 1);
+  const unsigned long long m = (1ull << (d.L & 0xFFu)) - 1ull;  // last digit of a clamped split
+  const bool clamped = !(d.L & 0x800u);
+  const unsigned long long fmin = dd == 0 ? 0ull : ((dd << 32) + mul - 1) / mul;
+  const unsigned long long fnext = (((dd + 1) << 32) + mul - 1) / mul;  // first f of the next digit
+  const unsigned long long maxw = word_max_u64<W>();
+  unsigned long long a, b = 0;
+  bool has_b = true;
+  if (sizeof(W) == 8 && sh >= 32) {
+    const unsigned long long lh = lo >> 32;
+    const int s2 = sh - 32;
+    const unsigned long long ah = lh + (fmin << s2), bh = lh + (fnext << s2);
+    a = ah > 0xFFFFFFFFull ? maxw : ah << 32;
+    if (bh > 0xFFFFFFFFull) has_b = false;
+    else b = (bh << 32) - 1ull;
+  } else {
+    const unsigned long long room = (maxw - lo) >> sh;  // largest f a word can have
+    a = fmin > room ? maxw : lo + (fmin << sh);
+    if (fnext > room || fnext >= 0xFFFFFFFFull) has_b = false;  // (>= 2^32 - 1: f may be saturated)
+    else b = lo + (fnext << sh) - 1ull;
+  }
+  if (!(clamped && dd == 0) && a > klo) klo = a;
+  if (has_b && !(clamped && dd >= m) && b < khi) khi = b;
+}
+
 // ---- kernels ---------------------------------------------------------------
 
 // Root setup: reset counters; the whole array becomes one split bucket or one
@@ -805,6 +888,8 @@ __device__ __forceinline__ void init_root(const Params<W>& P) {
     d.aux = 0;
     d.vbase = 0;
     d.bfirst = d.blast = 0;
+    d.klo = 0;
+    d.khi = word_max_u64<W>();
     P.split[0][0] = d;
     c->split_packed[0] = (1ull << 40) | (unsigned long long)ntiles_dev<W>(P.n);
   } else if (P.n > 1) {
@@ -896,10 +981,20 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
     // give no digit more than ~2x its share of the sample, classify by digit
     // (pure ALU) instead of by splitter search.  Radix buckets may split up
     // to 2^kMaxRadixL ways (no splitter table is needed).
-    const W srange = key_sub(shi, slo);
-    const int bl = key_bitlen(srange);
-    const int dshift = bl > 24 ? bl - 24 : 0;  // f = top 24 bits of (x - lo)
-    const unsigned long long rf = key_shr32(srange, dshift);
+    // The digits are tried first over the bucket's KNOWN bounds [klo, khi]
+    // (the word range at the root, a radix parent's digit cell below it):
+    // such a split needs no per-key clamps (classify_mode<5/6>); then over
+    // the sample's [min, max] (keys outside it clamp to the end digits).
+    W rlo = slo;       // digit origin
+    int dshift = 0;    // f = top 24 bits of (x - rlo)
+    unsigned long long rf = 0;
+    auto set_range = [&](const W& lo, const W& hi) {
+      const W range = key_sub(hi, lo);
+      const int bl = key_bitlen(range);
+      rlo = lo;
+      dshift = bl > 24 ? bl - 24 : 0;
+      rf = key_shr32(range, dshift);
+    };
     auto certify = [&](int D, unsigned long long& mul) -> bool {
       const int mr = D - 1;
       mul = ((unsigned long long)D << 32) / (rf + 1);
@@ -908,7 +1003,7 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
       if (threadIdx.x == 0) s_maxc = 0;
       __syncthreads();
       for (int i = threadIdx.x; i < S; i += THREADS)
-        atomicAdd(&dcnt[radix_digit(s[i], slo, dshift, (unsigned)mul, (unsigned)mr)], 1u);
+        atomicAdd(&dcnt[radix_digit(s[i], rlo, dshift, (unsigned)mul, (unsigned)mr)], 1u);
       __syncthreads();
       unsigned used = 0;
       for (int k = threadIdx.x; k <= mr; k += THREADS) {
@@ -941,7 +1036,23 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
     }
     unsigned long long dmul = 0;
     int Lf = L;
-    bool radix = certify(Dr, dmul);
+    bool radix = false, unc = false;
+    if constexpr (sizeof(W) <= 8) {
+      W blo, bhi;
+      {
+        const unsigned long long a = d.klo, b = d.khi;
+        memcpy(&blo, &a, sizeof(W));  // (little-endian low bytes)
+        memcpy(&bhi, &b, sizeof(W));
+      }
+      set_range(blo, bhi);
+      // (the high-word digit is exact only from an origin with a zero low word)
+      const bool ok = !(sizeof(W) == 8 && dshift >= 32 && (unsigned)d.klo != 0u);
+      if (ok) radix = unc = certify(Dr, dmul);
+    }
+    if (!radix) {
+      set_range(slo, shi);
+      radix = certify(Dr, dmul);
+    }
     if (radix) {
       Lf = 2;
       while ((1 << Lf) < Dr) ++Lf;
@@ -949,7 +1060,7 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
     unsigned meff = 0;  // distinct splitters when fewer than m (bits 24-31 of L)
     bool pw = false;    // piecewise radix over the splitters (bit 9 of L)
     if (radix) {
-      if (threadIdx.x == 0) g[0] = slo;
+      if (threadIdx.x == 0) g[0] = rlo;
     } else {
       // sort the S samples (padded to 4096 with the maximum) with the block
       // base-case sort, 512 threads x 8 keys, then stage them back to smem
@@ -1017,7 +1128,7 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
     if (threadIdx.x == 0) {
       // (tile cost weight 2 for every classifier but the plain radix digit: level_ranges)
       list[p].L = (unsigned)Lf | (radix ? (0x100u | ((unsigned)dshift << 16)) : 0x400u) | (pw ? 0x200u : 0u) |
-                  (meff << 24);
+                  (unc ? 0x800u : 0u) | (meff << 24);
       list[p].aux = dmul;
       atomicAdd(&P.ctrl->modes[P.level < 8 ? P.level : 7][radix ? 1 : (pw ? 2 : 0)], 1u);
     }
@@ -1267,6 +1378,12 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
     if (S.use_tree == 4) {
       if (X.flt) count_tile(std::integral_constant<int, 4>{}, std::true_type{});
       else count_tile(std::integral_constant<int, 4>{}, std::false_type{});
+    } else if (S.use_tree == 5) {
+      if (X.flt) count_tile(std::integral_constant<int, 5>{}, std::true_type{});
+      else count_tile(std::integral_constant<int, 5>{}, std::false_type{});
+    } else if (sizeof(W) == 8 && S.use_tree == 6) {
+      if (X.flt) count_tile(std::integral_constant<int, 6>{}, std::true_type{});
+      else count_tile(std::integral_constant<int, 6>{}, std::false_type{});
     } else if (sizeof(W) == 8 && S.use_tree == 3) {
       if (X.flt) count_tile(std::integral_constant<int, 3>{}, std::true_type{});
       else count_tile(std::integral_constant<int, 3>{}, std::false_type{});
@@ -1441,6 +1558,14 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
         nd.aux = 0;
         nd.vbase = 0;
         nd.bfirst = nd.blast = 0;
+        {
+          unsigned long long org = 0;  // the parent's digit origin (radix splits keep it in splitters[0])
+          if ((d.L & 0x100u) && sizeof(W) <= 8) {
+            const W g0 = P.splitters[(unsigned long long)p * 256];
+            memcpy(&org, &g0, sizeof(W) <= 8 ? sizeof(W) : 8);
+          }
+          child_bounds<W>(d, org, c, nd.klo, nd.khi);
+        }
         P.split[nxt][q] = nd;
       } else {
         P.ctrl->error = 1;
@@ -1673,7 +1798,9 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     // recompute child ids at write-out instead of staging them (cheap for
     // <= 32-bit words and the 64-bit high-word classifier; piecewise radix
     // stages them: f32 1e8 scatter@L0 0.39 -> 0.34 ms)
-    const bool radix = (sizeof(W) <= 4 && S.use_tree == 2) || (sizeof(W) == 8 && S.use_tree == 3);
+    const bool unc = S.use_tree >= 5;  // known-bounds digit
+    const bool radix = (sizeof(W) <= 4 && (S.use_tree == 2 || S.use_tree == 5)) ||
+                       (sizeof(W) == 8 && (S.use_tree == 3 || S.use_tree == 6));
     // bk[] holds each key's shared-histogram SLOT (hslot of its child id; the
     // digit itself in the radix modes), or -1 (wide cell) / -2 (past the tile)
     auto classify_tile = [&](auto tree_tag, auto flt_tag) {
@@ -1720,6 +1847,12 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     if (S.use_tree == 4) {
       if (X.flt) classify_tile(std::integral_constant<int, 4>{}, std::true_type{});
       else classify_tile(std::integral_constant<int, 4>{}, std::false_type{});
+    } else if (S.use_tree == 5) {
+      if (X.flt) classify_tile(std::integral_constant<int, 5>{}, std::true_type{});
+      else classify_tile(std::integral_constant<int, 5>{}, std::false_type{});
+    } else if (sizeof(W) == 8 && S.use_tree == 6) {
+      if (X.flt) classify_tile(std::integral_constant<int, 6>{}, std::true_type{});
+      else classify_tile(std::integral_constant<int, 6>{}, std::false_type{});
     } else if (sizeof(W) == 8 && S.use_tree == 3) {
       if (X.flt) classify_tile(std::integral_constant<int, 3>{}, std::true_type{});
       else classify_tile(std::integral_constant<int, 3>{}, std::false_type{});
@@ -1836,12 +1969,22 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
 #endif
     if (radix && out_xf == XF_NONE && cnt == TILE) {  // full tile: unrolled, no bounds
       const RadixReg<W> R(S);
+      if (unc) {
 #pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        const int j = i * THREADS + threadIdx.x;
-        const W v = staged[j];
-        chk(R.slot(v), j);
-        gptr[R.slot(v)][j] = v;
+        for (int i = 0; i < ITEMS; ++i) {
+          const int j = i * THREADS + threadIdx.x;
+          const W v = staged[j];
+          chk(R.template slot<true>(v), j);
+          gptr[R.template slot<true>(v)][j] = v;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const int j = i * THREADS + threadIdx.x;
+          const W v = staged[j];
+          chk(R.template slot<false>(v), j);
+          gptr[R.template slot<false>(v)][j] = v;
+        }
       }
     } else if (out_xf == XF_NONE && cnt == TILE) {
 #pragma unroll
@@ -1855,13 +1998,14 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
       if (out_xf == XF_NONE) {
         for (int j = threadIdx.x; j < cnt; j += THREADS) {
           const W v = staged[j];
-          chk(R.slot(v), j);
-          gptr[R.slot(v)][j] = v;
+          const int sl = unc ? R.template slot<true>(v) : R.template slot<false>(v);
+          chk(sl, j);
+          gptr[sl][j] = v;
         }
       } else {
         for (int j = threadIdx.x; j < cnt; j += THREADS) {
           const W v = staged[j];
-          gptr[R.slot(v)][j] = dec<W>(v, out_xf);
+          gptr[unc ? R.template slot<true>(v) : R.template slot<false>(v)][j] = dec<W>(v, out_xf);
         }
       }
     } else if (out_xf == XF_NONE) {
