@@ -1138,9 +1138,11 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
   __shared__ unsigned s_ticket;
   bool last = P.root_init != 0;  // (root level: CTA 0 is the only one here)
   if (!last) {
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_ticket = atomicAdd(&P.ctrl->sample_done, 1u);
+    if (threadIdx.x == 0) {
+      __threadfence();  // (after the barrier: orders the whole CTA's descriptor writes)
+      s_ticket = atomicAdd(&P.ctrl->sample_done, 1u);
+    }
     __syncthreads();
     last = s_ticket == gridDim.x - 1;
   }
@@ -1503,6 +1505,9 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
   const int nb = (int)(packed >> 40);
   const SplitDesc* list = P.split[P.cur];
   const int nxt = P.cur ^ 1;
+  // CTAs beyond the bucket count (most of the grid at the top levels) only
+  // scan tile counts into prefixes (below), concurrently with the bucket work
+  const bool spare = (int)gridDim.x > nb;
   for (int p = blockIdx.x; p < nb; p += gridDim.x) {
     const SplitDesc d = list[p];
     const int L = (int)(d.L & 0xFFu);
@@ -1656,8 +1661,11 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
   {
     const unsigned long long T = packed & kTileMask;
     const int lane = threadIdx.x & 31;
-    const unsigned long long nw = (unsigned long long)gridDim.x * (THREADS / 32);
-    for (unsigned long long t = (unsigned long long)blockIdx.x * (THREADS / 32) + (threadIdx.x >> 5); t < T; t += nw) {
+    // (with spare CTAs the bucket CTAs skip this pass: it then overlaps their work)
+    if (spare && (int)blockIdx.x < nb) return;
+    const unsigned long long first = spare ? (unsigned long long)((int)blockIdx.x - nb) : blockIdx.x;
+    const unsigned long long nw = (unsigned long long)(spare ? (int)gridDim.x - nb : (int)gridDim.x) * (THREADS / 32);
+    for (unsigned long long t = first * (THREADS / 32) + (threadIdx.x >> 5); t < T; t += nw) {
       uint4* row = reinterpret_cast<uint4*>(P.tilecnt + t * kChildStride) + 2 * lane;
       uint4 q[2] = {row[0], row[1]};
       unsigned* w = reinterpret_cast<unsigned*>(q);  // 8 words = 16 u16 counts
