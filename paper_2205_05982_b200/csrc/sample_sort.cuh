@@ -53,7 +53,7 @@ struct SplitDesc {
   unsigned long long aux;  // radix mode: digit multiplier M (digit = f * M >> 32)
   unsigned flags, L;       // L: bits 0-7 fan-out exponent, bit 8 radix mode, bit 9 piecewise
                            //    radix over the splitters, bit 10 tile cost weight - 1, bit 11 radix over the
-                           //    bucket's known bounds (unclamped digit),
+                           //    bucket's known bounds (unclamped digit), bit 12 log units (with bit 9),
                            //    bits 16-23 shift, bits 24-31 distinct splitter count when < 2^L - 1
   // Cost-weighted tile order of the level (k_sample's last CTA, level_ranges):
   // the bucket's tiles start at virtual position vbase and are `weight` units
@@ -89,7 +89,7 @@ struct Ctrl {
   unsigned long long partition_calls, keys_partitioned, base_cases;
   unsigned error;
   unsigned sample_done;  // k_sample CTAs finished (the last one lays out the level's CTA tile ranges)
-  unsigned modes[8][4];  // (diagnostics) buckets per level: splitter table/tree, radix, piecewise radix
+  unsigned modes[8][4];  // (diagnostics) buckets per level: splitter table/tree, radix, piecewise radix, ... over log units
 };
 
 // Compile-time configuration per key word: the classify/scatter tile (keys
@@ -372,7 +372,8 @@ struct SplSmem {
   int tdepth;     // tree mode: levels (2^tdepth - 1 >= m; shallow for few splitters)
   int shift, m, use_tree;  // use_tree: 0 table, 1 tree, 2 radix (equal-width digits),
                            //   3 radix on the high word (64-bit keys, shift >= 32), 4 piecewise
-                           //   radix, 5 / 6 = 2 / 3 over the bucket's known bounds (unclamped)
+                           //   radix, 5 / 6 = 2 / 3 over the bucket's known bounds (unclamped), 7 piecewise
+                           //   radix over log units (skewed integers)
   unsigned mul;  // radix mode multiplier (radix_digit)
   unsigned short lut[kLut];  // (first, end) splitter index of cell c, packed lo | hi << 8
 };
@@ -401,6 +402,32 @@ __device__ __forceinline__ void fine_geometry(const W& range, int& rsh, int& lsh
   rsh = bl > kL1Bits + kSubBits ? bl - (kL1Bits + kSubBits) : 0;
   lsh = bl < kL1Bits + kSubBits ? kL1Bits + kSubBits - bl : 0;
   cmax = key_shr32(range, rsh);
+}
+
+// Log-scale fine units (piecewise radix over skewed integers, use_tree 7):
+// the unit of y = x - lo is y itself below 2^(kLogM+1), else (bit length,
+// top kLogM bits below the leading one) -- a minifloat code of y, monotone
+// and < 2^21 for every word type.  Power-law / log-uniform keys (e.g.
+// floor(2^64 u^4)) have a smooth density per "exponent band" of this code, as
+// floats have in theirs, so equal-width digits inside each first-level bucket
+// balance where linear units put most splitters into one bucket.
+constexpr int kLogM = 14;
+template <typename W>
+__device__ __forceinline__ unsigned log_unit_of(const W& y) {
+  const int e = key_bitlen(y);
+  if (e <= kLogM + 1) return key_shr32(y, 0);
+  return ((unsigned)(e - kLogM) << kLogM) | (key_shr32(y, e - 1 - kLogM) & ((1u << kLogM) - 1u));
+}
+template <typename W>
+__device__ __forceinline__ unsigned fine_unit_log(const W& x, const W& lo, unsigned cmax) {
+  const unsigned cf = log_unit_of(key_sub(x, lo));
+  return key_lt(x, lo) ? 0u : (cf < cmax ? cf : cmax);
+}
+// First key of log unit u (false if beyond hi).
+template <typename W>
+__device__ __forceinline__ bool unit_start_log(const W& lo, const W& hi, unsigned u, W& out) {
+  if (u < (2u << kLogM)) return cell_start<W>(lo, hi, u, 0, out);
+  return cell_start<W>(lo, hi, (1u << kLogM) | (u & ((1u << kLogM) - 1u)), (int)(u >> kLogM) - 1, out);
 }
 
 // (first, end) splitter pair of key x's table cell.  A first-level bucket
@@ -433,10 +460,10 @@ __device__ __forceinline__ int lower_bound_smem(const W* srt, int lo, int hi, co
 // bucket (normal floats: a bucket is at most one exponent band), so children
 // stay balanced with one near-broadcast table load per key and no splitter
 // compare.  Digits lie in [0, m).
-template <typename W>
+template <bool LOG = false, typename W>
 __device__ __forceinline__ unsigned pw_digit(const W& x, const W& lo, int rsh, int lsh, unsigned cmax,
                                              const unsigned* t1) {
-  const unsigned cf = fine_unit(x, lo, rsh, lsh, cmax);
+  const unsigned cf = LOG ? fine_unit_log(x, lo, cmax) : fine_unit(x, lo, rsh, lsh, cmax);
   const unsigned t = t1[cf >> kSubBits];
   return (t & 0xFFFFu) + (((cf & ((1u << kSubBits) - 1)) * (t >> 16)) >> kSubBits);
 }
@@ -446,15 +473,16 @@ __device__ __forceinline__ unsigned pw_digit(const W& x, const W& lo, int rsh, i
 // (and a barrier followed).  Returns the bucket count.
 template <typename W>
 __device__ __forceinline__ int build_t1(const W* srt, int m, const W& lo, const W& hi, int rsh, int lsh,
-                                        unsigned cmax, unsigned* t1) {
+                                        unsigned cmax, unsigned* t1, bool logu = false) {
   const int n1 = (int)((cmax << lsh) >> kSubBits) + 1;
+  auto ustart = [&](unsigned u, W& out) {
+    return logu ? unit_start_log<W>(lo, hi, u, out) : unit_start<W>(lo, hi, u, rsh, lsh, out);
+  };
   for (int j = threadIdx.x; j < n1; j += blockDim.x) {
     W s0, s1;
-    const unsigned f0 =
-        unit_start<W>(lo, hi, (unsigned)j << kSubBits, rsh, lsh, s0) ? lower_bound_smem(srt, 0, m, s0) : m;
-    const unsigned f1 = (j + 1 < n1 && unit_start<W>(lo, hi, (unsigned)(j + 1) << kSubBits, rsh, lsh, s1))
-                            ? lower_bound_smem(srt, 0, m, s1)
-                            : (unsigned)m;
+    const unsigned f0 = ustart((unsigned)j << kSubBits, s0) ? lower_bound_smem(srt, 0, m, s0) : m;
+    const unsigned f1 = (j + 1 < n1 && ustart((unsigned)(j + 1) << kSubBits, s1)) ? lower_bound_smem(srt, 0, m, s1)
+                                                                                  : (unsigned)m;
     t1[j] = f0 | ((f1 - f0) << 16);
   }
   __syncthreads();
@@ -557,6 +585,18 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, unsigned lraw, Sp
     return;
   }
   const W lo = S.lo, hi = S.srt[m - 1];
+  if ((lraw & 0x1200u) == 0x1200u) {  // piecewise radix over log units (certified by k_sample)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      S.shift = 0;
+      S.lshift = 0;
+      S.cmax = log_unit_of(key_sub(hi, lo));
+      S.use_tree = 7;
+    }
+    __syncthreads();
+    build_t1(S.srt, m, lo, hi, 0, 0, S.cmax, S.t1, true);
+    return;
+  }
   const int sh = S.shift, lsh = S.lshift;
   const int n1 = build_t1(S.srt, m, lo, hi, sh, lsh, S.cmax, S.t1);
   if (lraw & 0x200u) {  // piecewise radix (certified by k_sample): t1 is the whole classifier
@@ -627,7 +667,9 @@ __device__ __forceinline__ void load_splitters(const W* g_srt, unsigned lraw, Sp
 // lands in equality bucket 2m+1).
 template <int MODE, typename W>
 __device__ __forceinline__ int classify_mode(const W& x, const SplSmem<W>& S) {
-  if constexpr (MODE == 6 && sizeof(W) == 8) {
+  if constexpr (MODE == 7) {
+    return 2 * (int)pw_digit<true>(x, S.lo, 0, 0, S.cmax, S.t1);
+  } else if constexpr (MODE == 6 && sizeof(W) == 8) {
     return 2 * (int)radix_digit_unc_hi(x, S.lo, S.shift, S.mul);
   } else if constexpr (MODE >= 5) {
     return 2 * (int)radix_digit_unc(x, S.lo, S.shift, S.mul);
@@ -696,7 +738,8 @@ struct RadixReg {
 
 template <typename W>
 __device__ __forceinline__ int classify_fast(const W& x, const SplSmem<W>& S) {
-  return S.use_tree == 6 ? classify_mode<6>(x, S)
+  return S.use_tree == 7 ? classify_mode<7>(x, S)
+         : S.use_tree == 6 ? classify_mode<6>(x, S)
          : S.use_tree == 5 ? classify_mode<5>(x, S)
          : S.use_tree == 4 ? classify_mode<4>(x, S)
          : S.use_tree == 3 ? classify_mode<3>(x, S)
@@ -1059,6 +1102,7 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
     }
     unsigned meff = 0;  // distinct splitters when fewer than m (bits 24-31 of L)
     bool pw = false;    // piecewise radix over the splitters (bit 9 of L)
+    bool pwlog = false; // ... over log units (bit 12 of L)
     if (radix) {
       if (threadIdx.x == 0) g[0] = rlo;
     } else {
@@ -1123,14 +1167,33 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
         for (int k2 = threadIdx.x; k2 < mq; k2 += THREADS) atomicMax(&s_maxc, dcnt[k2]);
         __syncthreads();
         pw = (unsigned)s_maxc * (unsigned)mq <= 2u * (unsigned)S + 4u * (unsigned)mq;
+        // Skewed integers (power-law / log-uniform keys put most splitters
+        // into one linear first-level bucket): the same test over LOG units
+        // (fine_unit_log).  Encoded keys only -- raw floats certify above.
+        if (!pw && xf < XF_FLT_ASC) {
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            s_pwcmax = log_unit_of(key_sub(s_spl[mq - 1], s_spl[0]));
+            s_maxc = 0;
+          }
+          for (int k2 = threadIdx.x; k2 < mq; k2 += THREADS) dcnt[k2] = 0;
+          __syncthreads();
+          build_t1(s_spl, mq, s_pwlo, s_spl[mq - 1], 0, 0, s_pwcmax, s_t1, true);
+          for (int i = threadIdx.x; i < S; i += THREADS)
+            atomicAdd(&dcnt[pw_digit<true>(s[i], s_pwlo, 0, 0, s_pwcmax, s_t1)], 1u);
+          __syncthreads();
+          for (int k2 = threadIdx.x; k2 < mq; k2 += THREADS) atomicMax(&s_maxc, dcnt[k2]);
+          __syncthreads();
+          pwlog = pw = (unsigned)s_maxc * (unsigned)mq <= 2u * (unsigned)S + 4u * (unsigned)mq;
+        }
       }
     }
     if (threadIdx.x == 0) {
       // (tile cost weight 2 for every classifier but the plain radix digit: level_ranges)
       list[p].L = (unsigned)Lf | (radix ? (0x100u | ((unsigned)dshift << 16)) : 0x400u) | (pw ? 0x200u : 0u) |
-                  (unc ? 0x800u : 0u) | (meff << 24);
+                  (unc ? 0x800u : 0u) | (pwlog ? 0x1000u : 0u) | (meff << 24);
       list[p].aux = dmul;
-      atomicAdd(&P.ctrl->modes[P.level < 8 ? P.level : 7][radix ? 1 : (pw ? 2 : 0)], 1u);
+      atomicAdd(&P.ctrl->modes[P.level < 8 ? P.level : 7][radix ? 1 : (pwlog ? 3 : (pw ? 2 : 0))], 1u);
     }
     __syncthreads();
   }
@@ -1380,6 +1443,8 @@ __global__ void __launch_bounds__(Cfg<W>::kHistThreads, Cfg<W>::kHistMinBlocks) 
     if (S.use_tree == 4) {
       if (X.flt) count_tile(std::integral_constant<int, 4>{}, std::true_type{});
       else count_tile(std::integral_constant<int, 4>{}, std::false_type{});
+    } else if (S.use_tree == 7) {  // (log units: integer keys only -- floats certify the linear units)
+      count_tile(std::integral_constant<int, 7>{}, std::false_type{});
     } else if (S.use_tree == 5) {
       if (X.flt) count_tile(std::integral_constant<int, 5>{}, std::true_type{});
       else count_tile(std::integral_constant<int, 5>{}, std::false_type{});
@@ -1855,6 +1920,8 @@ __global__ void __launch_bounds__(Cfg<W>::kScatThreads, Cfg<W>::kScatMinBlocks) 
     if (S.use_tree == 4) {
       if (X.flt) classify_tile(std::integral_constant<int, 4>{}, std::true_type{});
       else classify_tile(std::integral_constant<int, 4>{}, std::false_type{});
+    } else if (S.use_tree == 7) {  // (log units: integer keys only -- floats certify the linear units)
+      classify_tile(std::integral_constant<int, 7>{}, std::false_type{});
     } else if (S.use_tree == 5) {
       if (X.flt) classify_tile(std::integral_constant<int, 5>{}, std::true_type{});
       else classify_tile(std::integral_constant<int, 5>{}, std::false_type{});

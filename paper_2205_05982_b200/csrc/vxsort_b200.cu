@@ -578,8 +578,8 @@ vxs_status run_sort(W* keys, size_t n, int xf, uint64_t seed, void* ws, size_t w
                  h.item_count[kListCopySmall], h.item_count[kListCopyBig]);
   if (std::getenv("VXSORT_TRACE"))
     for (int l = 0; l < levels && l < 8; ++l)
-      std::fprintf(stderr, "  level %d buckets: splitters %u radix %u piecewise %u\n", l, h.modes[l][0], h.modes[l][1],
-                   h.modes[l][2]);
+      std::fprintf(stderr, "  level %d buckets: splitters %u radix %u piecewise %u piecewise-log %u\n", l, h.modes[l][0],
+                   h.modes[l][1], h.modes[l][2], h.modes[l][3]);
   ProfScope phase(K_FINAL_PHASE, st);  // (closes at the end of run_sort's final block)
   // The size classes and the equality-bucket copy touch disjoint items: the
   // class holding the most keys runs on the caller's stream, the rest on a

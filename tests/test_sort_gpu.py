@@ -202,3 +202,22 @@ def test_clustered_keys_outside_sample_range(cuda):
     k128[:, 1] = rng.integers(0, 2**64, n // 2, dtype=np.uint64)
     k128[: n // 4, 1] &= np.uint64(0xFF)
     check(k128, "k128", False)
+
+
+def test_skewed_keys_log_units(cuda):
+    # power-law keys (C5's u^4 skew; also u^8 and log-uniform): the piecewise
+    # radix over log units (fine_unit_log) must stay bit-exact for every word
+    rng = np.random.default_rng(11)
+    n = 3_000_000
+    u = rng.random(n)
+    for name, f in (("u4", u ** 4), ("u8", u ** 8), ("logu", np.exp2(-40.0 * u))):
+        x64 = np.minimum(np.floor(np.ldexp(f, 64)), float(2**64 - 2**11)).astype(np.uint64)
+        for desc in (False, True):
+            check(x64, "u64", desc)
+            check((x64 >> np.uint64(32)).astype(np.uint32), "u32", desc)
+            check((x64 >> np.uint64(1)).astype(np.int64) - np.int64(2**40), "i64", desc)
+        k = np.empty((n // 4, 2), np.uint64)
+        k[:, 1] = x64[: n // 4]
+        k[:, 0] = rng.integers(0, 2**64, n // 4, dtype=np.uint64)
+        check(k, "k128", False)
+        check((x64 >> np.uint64(48)).astype(np.uint16), "u16", False)
