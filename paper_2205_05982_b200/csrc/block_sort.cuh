@@ -329,7 +329,6 @@ template <typename W, int THREADS, int ITEMS, bool FLT, bool RANK>
 __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, W* dst, const Xf<W>& X) {
   using BS = BinSort<W, THREADS, ITEMS>;
   constexpr int TOTAL = BS::kTotal;
-  constexpr int NB = BS::kNB;
   constexpr int NW = THREADS / 32;
   constexpr int NV = ITEMS * (int)sizeof(W) / 16;  // uint4 per thread row
   static_assert(NV * 16 == ITEMS * (int)sizeof(W), "vector rows");
@@ -366,18 +365,23 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, W* 
   unsigned mx = 0;  // largest bin (RANK: largest rank)
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
+    // (padding slots take no part in the counting: they keep their own
+    // positions [size, TOTAL) in pass 2 -- no same-address atomics on a
+    // dummy bin, up to a third of the slots of a half-full item)
     const bool valid = i * THREADS + tid < size;
-    const unsigned b = valid ? bin_of(k[i]) : (unsigned)(NB + BS::kBinsPerWord);
+    const unsigned b = bin_of(k[i]);
     const int w = BS::kPacked ? BS::wslot((int)(b >> 1)) : BS::wslot((int)b);
     const unsigned h = BS::kPacked ? (b & 1u) << 4 : 0u;
     br[i] = ((unsigned)w << 17) | ((h >> 4) << 16);
-    if constexpr (RANK) {
-      const unsigned r = (atomicAdd(&cnt[w], 1u << h) >> h) & 0xFFFFu;
-      br[i] |= r;
-      sq += 2u * r + 1u;  // sum over keys of 2*rank + 1 = sum over bins of count^2
-      mx = valid ? umax(mx, r) : mx;
-    } else {
-      atomicAdd(&cnt[w], 1u << h);
+    if (valid) {
+      if constexpr (RANK) {
+        const unsigned r = (atomicAdd(&cnt[w], 1u << h) >> h) & 0xFFFFu;
+        br[i] |= r;
+        sq += 2u * r + 1u;  // sum over keys of 2*rank + 1 = sum over bins of count^2
+        mx = umax(mx, r);
+      } else {
+        atomicAdd(&cnt[w], 1u << h);
+      }
     }
   }
   __syncthreads();
@@ -434,8 +438,6 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, W* 
   }
   if constexpr (RANK) {
     rounds += 1;  // largest rank + 1 = largest bin
-    const unsigned pad = (unsigned)(TOTAL - size);  // the padding bin adds pad^2
-    tsq -= pad * pad;
   }
   // block-uniform rejection; cnt is no longer read
   if (tsq > 4u * (unsigned)size + 256u || rounds > (unsigned)BS::kMaxBin) return false;
@@ -469,14 +471,20 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, W* 
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const unsigned h = ((br[i] >> 16) & 1u) << 4;
-    unsigned pos;
-    if constexpr (RANK) pos = ((cnt[br[i] >> 17] >> h) & 0xFFFFu) + (br[i] & 0xFFFFu);
-    else pos = (atomicAdd(&cnt[br[i] >> 17], 1u << h) >> h) & 0xFFFFu;
-    VXS_DCHECK(pos < (unsigned)TOTAL, "base case: bin slot outside the item");
-    sk[BS::swz((int)pos)] = i * THREADS + tid < size ? k[i] : key_max<W>();
+    const bool valid = i * THREADS + tid < size;
+    unsigned pos = (unsigned)(i * THREADS + tid);  // (padding: its own slot, >= size)
+    if (valid) {
+      if constexpr (RANK) pos = ((cnt[br[i] >> 17] >> h) & 0xFFFFu) + (br[i] & 0xFFFFu);
+      else pos = (atomicAdd(&cnt[br[i] >> 17], 1u << h) >> h) & 0xFFFFu;
+    }
+    VXS_DCHECK(pos < (unsigned)TOTAL && (valid ? pos < (unsigned)size : true), "base case: bin slot outside the item");
+    sk[BS::swz((int)pos)] = valid ? k[i] : key_max<W>();
   }
   __syncthreads();
   // odd-even transposition rounds over this thread's row of ITEMS positions
+  // (a warp whose 32 rows hold only padding -- the tail of a part-full item --
+  // skips the rounds: the shuffles below stay inside the warp)
+  const bool live = warp * 32 * ITEMS < size;  // (warp-uniform)
   W v[ITEMS];
   {
     const uint4* row = reinterpret_cast<const uint4*>(sk);
@@ -486,7 +494,7 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, W* 
       memcpy(reinterpret_cast<char*>(v) + 16 * q, &t, 16);
     }
   }
-  if (rounds > 1) {
+  if (rounds > 1 && live) {
 #pragma unroll 1
     for (unsigned r = 0; r < rounds; r += 2) {
 #pragma unroll
@@ -500,7 +508,7 @@ __device__ __forceinline__ bool bin_sort_item(const W (&k)[ITEMS], int size, W* 
       if (lane > 0 && key_lt(v[0], pv)) v[0] = pv;
     }
   }
-  {
+  if (rounds > 1 && live) {
     uint4* row = reinterpret_cast<uint4*>(sk);
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
