@@ -52,7 +52,7 @@ struct SplitDesc {
   unsigned long long start, size, tile_base;
   unsigned long long aux;  // radix mode: digit multiplier M (digit = f * M >> 32)
   unsigned flags, L;       // L: bits 0-7 fan-out exponent, bit 8 radix mode, bit 9 piecewise
-                           //    radix over the splitters, bit 10 tile cost weight - 1, bit 11 radix over the
+                           //    radix over the splitters, bits 10 / 13 tile cost weight (tile_weight), bit 11 radix over the
                            //    bucket's known bounds (unclamped digit), bit 12 log units (with bit 9),
                            //    bits 16-23 shift, bits 24-31 distinct splitter count when < 2^L - 1
   // Cost-weighted tile order of the level (k_sample's last CTA, level_ranges):
@@ -68,14 +68,16 @@ struct SplitDesc {
   // clamps (L bit 11, classify_mode<5/6>).
   unsigned long long klo, khi;
 };
-constexpr unsigned kMaxTileWeight = 2;  // (k_sample sets weight 1 or 2)
+constexpr unsigned kMaxTileWeight = 3;  // (k_sample: plain radix 1, piecewise radix 2, splitter table / tree 3)
 // Largest word value as u64 (bucket bounds; 16-byte words carry none).
 template <typename W>
 __host__ __device__ __forceinline__ unsigned long long word_max_u64() {
   if constexpr (sizeof(W) >= 8) return ~0ull;
   else return (1ull << (8 * sizeof(W))) - 1ull;
 }
-__host__ __device__ __forceinline__ unsigned tile_weight(unsigned L) { return ((L >> 10) & 1u) + 1u; }
+__host__ __device__ __forceinline__ unsigned tile_weight(unsigned L) {
+  return 1u + ((L >> 10) & 1u) + 2u * ((L >> 13) & 1u);
+}
 
 struct Item {
   unsigned long long start, size;
@@ -1189,8 +1191,10 @@ __global__ void __launch_bounds__(THREADS) k_sample(Params<W> P) {
       }
     }
     if (threadIdx.x == 0) {
-      // (tile cost weight 2 for every classifier but the plain radix digit: level_ranges)
-      list[p].L = (unsigned)Lf | (radix ? (0x100u | ((unsigned)dshift << 16)) : 0x400u) | (pw ? 0x200u : 0u) |
+      // (tile cost weight: plain radix digit 1, piecewise radix 2 (bit 10), splitter
+      // table / tree 3 (bit 13) -- level_ranges)
+      list[p].L = (unsigned)Lf | (radix ? (0x100u | ((unsigned)dshift << 16)) : (pw ? 0x400u : 0x2000u)) |
+                  (pw ? 0x200u : 0u) |
                   (unc ? 0x800u : 0u) | (pwlog ? 0x1000u : 0u) | (meff << 24);
       list[p].aux = dmul;
       atomicAdd(&P.ctrl->modes[P.level < 8 ? P.level : 7][radix ? 1 : (pwlog ? 3 : (pw ? 2 : 0))], 1u);
