@@ -1565,7 +1565,8 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
   __shared__ unsigned long long s_off[kChildStride];
   __shared__ unsigned long long scan_scratch[32];
   __shared__ unsigned char s_kind[kChildStride];
-  __shared__ unsigned long long s_res[kNumLists];
+  __shared__ unsigned s_res[kNumLists];  // (32-bit: a 64-bit shared atomicAdd is a CAS loop -- with every
+                                         // child of a bucket on one list it was a quarter of this kernel)
   __shared__ unsigned long long s_base[kNumLists];
   __shared__ unsigned long long s_nsort;
   __shared__ unsigned long long s_split_base;
@@ -1689,7 +1690,7 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
     if (c < kNumLists) s_res[c] = 0;
     __syncthreads();
     unsigned long long my_slot = 0;
-    if (my_list >= 0) my_slot = atomicAdd(&s_res[my_list], 1ull);
+    if (my_list >= 0) my_slot = atomicAdd(&s_res[my_list], 1u);
     __syncthreads();
     if (c < kNumLists) {
       const unsigned long long k = s_res[c];
