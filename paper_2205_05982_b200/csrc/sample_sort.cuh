@@ -1735,28 +1735,46 @@ __global__ void __launch_bounds__(kChildStride) k_plan(Params<W> P) {
     if (spare && (int)blockIdx.x < nb) return;
     const unsigned long long first = spare ? (unsigned long long)((int)blockIdx.x - nb) : blockIdx.x;
     const unsigned long long nw = (unsigned long long)(spare ? (int)gridDim.x - nb : (int)gridDim.x) * (THREADS / 32);
-    for (unsigned long long t = first * (THREADS / 32) + (threadIdx.x >> 5); t < T; t += nw) {
-      uint4* row = reinterpret_cast<uint4*>(P.tilecnt + t * kChildStride) + 2 * lane;
-      uint4 q[2] = {row[0], row[1]};
-      unsigned* w = reinterpret_cast<unsigned*>(q);  // 8 words = 16 u16 counts
-      unsigned sum = 0;
+    // (kU tiles per warp in flight: the loads of all of them are issued
+    // before the first scan -- a warp otherwise walks its tiles one global
+    // round trip at a time)
+    constexpr int kU = 4;
+    for (unsigned long long t0 = first * (THREADS / 32) + (threadIdx.x >> 5); t0 < T; t0 += kU * nw) {
+      uint4 q[kU][2];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) sum += (w[j] & 0xFFFFu) + (w[j] >> 16);
-      unsigned incl = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+      for (int u = 0; u < kU; ++u) {
+        const unsigned long long t = t0 + u * nw;
+        if (t < T) {
+          const uint4* row = reinterpret_cast<const uint4*>(P.tilecnt + t * kChildStride) + 2 * lane;
+          q[u][0] = row[0];
+          q[u][1] = row[1];
+        }
       }
-      unsigned run = incl - sum;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const unsigned a = w[j] & 0xFFFFu, b = w[j] >> 16;
-        w[j] = (run & 0xFFFFu) | ((run + a) << 16);
-        run += a + b;
+      for (int u = 0; u < kU; ++u) {
+        const unsigned long long t = t0 + u * nw;
+        if (t >= T) break;  // (warp-uniform)
+        unsigned* w = reinterpret_cast<unsigned*>(q[u]);  // 8 words = 16 u16 counts
+        unsigned sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sum += (w[j] & 0xFFFFu) + (w[j] >> 16);
+        unsigned incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        unsigned run = incl - sum;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const unsigned a = w[j] & 0xFFFFu, b = w[j] >> 16;
+          w[j] = (run & 0xFFFFu) | ((run + a) << 16);
+          run += a + b;
+        }
+        uint4* row = reinterpret_cast<uint4*>(P.tilecnt + t * kChildStride) + 2 * lane;
+        row[0] = q[u][0];
+        row[1] = q[u][1];
       }
-      row[0] = q[0];
-      row[1] = q[1];
     }
   }
 }
