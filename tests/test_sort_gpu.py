@@ -221,3 +221,20 @@ def test_skewed_keys_log_units(cuda):
         k[:, 0] = rng.integers(0, 2**64, n // 4, dtype=np.uint64)
         check(k, "k128", False)
         check((x64 >> np.uint64(48)).astype(np.uint16), "u16", False)
+
+
+@pytest.mark.parametrize("kt", ["i32", "u32", "f32", "i64", "u64", "f64", "k128", "i16"])
+def test_two_levels_every_word_vs_oracle(cuda, kt):
+    # 5e6 keys: two levels (known-bounds radix below a radix parent, weighted
+    # CTA tile ranges, per-tile prefixes), bit-exact against the oracle
+    rng = np.random.default_rng(hash(kt) & 0xFFF)
+    n = 5_000_000
+    x = rand_keys(kt, n, rng)
+    for desc in (False, True):
+        st = check(x, kt, desc)
+        if kt != "i16":  # (65536 distinct values end in equality buckets after one level)
+            assert st.max_depth >= 2
+    if kt in ("u32", "u64", "i64"):  # a narrow range off the word boundaries: clamped digits at the root
+        lo = 123456789
+        y = (rand_keys("u32", n, rng).astype(np.uint64) % np.uint64(3_000_000_000) + np.uint64(lo)).astype(NP[kt])
+        check(y, kt, False)
