@@ -15,7 +15,9 @@ import paper_2205_05982_b200 as vx  # noqa: E402
 
 rng = np.random.default_rng(3)
 cases = [("u32", 200_000, False), ("u64", 150_000, True), ("f32", 120_000, False), ("i16", 70_000, True),
-         ("k128", 60_000, False), ("u64", 3_000, False), ("u32", 1_500_000, False)]
+         ("k128", 60_000, False), ("u64", 3_000, False), ("u32", 1_500_000, False),
+         # two levels: known-bounds digits below a radix parent, weighted CTA ranges, tile prefixes
+         ("u32", 3_000_000, True), ("u64", 3_000_000, False), ("f32", 3_000_000, True)]
 ok = True
 for kt, n, desc in cases:
     if kt == "k128":
@@ -35,6 +37,14 @@ for kt, n, desc in cases:
     good = d.cpu().numpy().tobytes() == want.tobytes()
     ok &= good
     print(kt, n, desc, "ok" if good else "MISMATCH", flush=True)
+# power-law keys: piecewise radix over log units, then known-bounds / clamped digits below it
+u = rng.random(3_000_000)
+x = np.minimum(np.floor(np.ldexp(u ** 4, 64)), float(2**64 - 2**11)).astype(np.uint64)
+d = torch.from_numpy(x.copy()).cuda()
+vx.sort(d, vx.SortConfig(seed=1))
+good = d.cpu().numpy().tobytes() == oracle.sort(x, "u64")[0].tobytes()
+ok &= good
+print("u64 skew", "ok" if good else "MISMATCH", flush=True)
 # clustered keys -> counting-sort rejection -> network fallback
 x = (rng.integers(0, 50, 100_000, dtype=np.uint64) << np.uint64(40)) | rng.integers(0, 3, 100_000, dtype=np.uint64)
 d = torch.from_numpy(x.copy()).cuda()
