@@ -354,6 +354,18 @@ template <typename W>
 __device__ __forceinline__ unsigned radix_digit_unc(const W& x, const W& lo, int shift, unsigned mul) {
   return __umulhi(key_shr32(key_sub(x, lo), shift), mul);
 }
+// (<= 32-bit words: the shift is < 32 -- at most 8 -- so no guarded shift)
+__device__ __forceinline__ unsigned radix_digit_unc(const uint32_t& x, const uint32_t& lo, int shift, unsigned mul) {
+  return __umulhi((x - lo) >> shift, mul);
+}
+__device__ __forceinline__ unsigned radix_digit_unc(const uint16_t& x, const uint16_t& lo, int shift, unsigned mul) {
+  return __umulhi((unsigned)(uint16_t)(x - lo) >> shift, mul);
+}
+// (64-bit words below the high-word mode: shift < 32 and (x - lo) >> shift < 2^25, no saturation)
+__device__ __forceinline__ unsigned radix_digit_unc(const unsigned long long& x, const unsigned long long& lo, int shift,
+                                                    unsigned mul) {
+  return __umulhi((unsigned)((x - lo) >> shift), mul);
+}
 // Same on the high words (64-bit keys, shift >= 32; lo has a zero low word,
 // so hi(x) - hi(lo) is exact).
 __device__ __forceinline__ unsigned radix_digit_unc_hi(unsigned long long x, unsigned long long lo, int shift,
