@@ -882,6 +882,10 @@ __global__ void k_gather(const W* a, W* b, GatherSet g) {
 // H2D, one device sort, one D2H).
 void pipe_dims(size_t n, size_t kb, int& C, int& S) {
   const size_t bytes = n * kb;
+  // (16 chunks: swept 4-32 on 400 MB.  Pinned sources are within noise from
+  // 6 to 16 -- fewer chunks shorten the run of small tail sorts, more merge
+  // rounds cost nothing visible -- and the staged pageable path needs the
+  // finer pipelining: 20.3 ms with 16 chunks against 25.6 with 8)
   C = bytes >= (size_t(64) << 20) ? 16 : 1;
   S = bytes >= (size_t(256) << 20) ? 64 : 32;
   if (const char* e = std::getenv("VXSORT_HOST_CHUNKS")) C = std::atoi(e);
@@ -1004,6 +1008,27 @@ vxs_status host_pipeline(PipeCtx& X, W* h, size_t n, int xf, uint64_t seed, int 
       qh = (qh + 1) % kStageSlots;
       --qn;
     };
+    if (!staged) {
+      // Pinned destination: slices leave in groups of 1, 1, 2, 4, 8, ... --
+      // one cudaMemcpyAsync per group.  The merges run several times faster
+      // than PCIe drains them, so only the first slices are latency-critical;
+      // 64 separate copies cost ~0.5 ms of per-copy overhead on a 7.2 ms D2H.
+      int s = 0, gsz = 1, ngroups = 0;
+      while (s < S) {
+        const int s1 = std::min(S, s + gsz);
+        out_ready.wait(s1);
+        const unsigned long long b0 = sl_off[s], b1 = sl_off[s1];
+        if (b1 > b0 && thread_err[1] == cudaSuccess) {
+          for (int j = s; j < s1; ++j)
+            if (sl_off[j + 1] > sl_off[j]) cudaStreamWaitEvent(X.s_out, X.ev_sl[j], 0);
+          const cudaError_t ce = cudaMemcpyAsync(h + b0, B + b0, (b1 - b0) * sizeof(W), cudaMemcpyDeviceToHost, X.s_out);
+          if (ce != cudaSuccess) thread_err[1] = ce;
+        }
+        s = s1;
+        if (++ngroups >= 2) gsz *= 2;
+      }
+      return;
+    }
     for (int s = 0; s < S; ++s) {
       out_ready.wait(s + 1);
       const unsigned long long len = sl_off[s + 1] - sl_off[s];
@@ -1035,6 +1060,7 @@ vxs_status host_pipeline(PipeCtx& X, W* h, size_t n, int xf, uint64_t seed, int 
     while (qn) drain_one();
   });
   // 1b. sort each chunk as it lands
+  std::vector<cudaEvent_t> tcs;  // (trace: per-chunk sort completion)
   for (int c = 0; c < C; ++c) {
     in_ready.wait(c + 1);
     if (st != VXS_OK) continue;
@@ -1043,6 +1069,12 @@ vxs_status host_pipeline(PipeCtx& X, W* h, size_t n, int xf, uint64_t seed, int 
     st = run_sort<W>(A + cs.off[c], cs.off[c + 1] - cs.off[c], xf, seed + (uint64_t)c * 0x9E3779B97F4A7C15ull,
                      nullptr, 0, X.s_cmp, &sc);
     add_stats(acc, sc);
+    if (trace) {
+      cudaEvent_t ev;
+      cudaEventCreate(&ev);
+      cudaEventRecord(ev, X.s_cmp);
+      tcs.push_back(ev);
+    }
   }
   // 2. global splitters from a regular sample of the sorted chunks; bounds
   std::vector<unsigned long long> hb((size_t)C * (S + 1), 0);
@@ -1151,6 +1183,14 @@ vxs_status host_pipeline(PipeCtx& X, W* h, size_t n, int xf, uint64_t seed, int 
     std::fprintf(stderr,
                  "[vxsort pipe C=%d S=%d %s] h2d %.3f  chunk-sorts %.3f  bounds %.3f  slice0 %.3f  d2h-done %.3f ms\n",
                  C, S, staged ? "staged" : "pinned", t[1], t[2], t[3], t[4], t[5]);
+    std::fprintf(stderr, "  chunk sorts done at (ms):");
+    for (auto& ev : tcs) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, tev[0], ev);
+      std::fprintf(stderr, " %.2f", ms);
+      cudaEventDestroy(ev);
+    }
+    std::fprintf(stderr, "\n");
     for (auto& x : tev) cudaEventDestroy(x);
   }
   cudaStreamWaitEvent(X.s_cmp, X.ev_done, 0);
