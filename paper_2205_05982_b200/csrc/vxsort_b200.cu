@@ -1059,15 +1059,23 @@ vxs_status host_pipeline(PipeCtx& X, W* h, size_t n, int xf, uint64_t seed, int 
     }
     while (qn) drain_one();
   });
-  // 1b. sort each chunk as it lands
+  // 1b. sort each chunk as it lands (one workspace for all the chunk sorts:
+  //     no stream-ordered alloc / free pair per chunk)
   std::vector<cudaEvent_t> tcs;  // (trace: per-chunk sort completion)
+  unsigned char* cws = nullptr;
+  size_t cws_bytes = 0;
+  for (int c = 0; c < C; ++c) cws_bytes = std::max(cws_bytes, layout_for<W>(cs.off[c + 1] - cs.off[c]).total);
+  if (st == VXS_OK) {
+    e = lib_malloc_async(reinterpret_cast<void**>(&cws), cws_bytes, X.s_cmp);
+    if (e != cudaSuccess) st = cuda_fail(e, "pipeline workspace alloc");
+  }
   for (int c = 0; c < C; ++c) {
     in_ready.wait(c + 1);
     if (st != VXS_OK) continue;
     cudaStreamWaitEvent(X.s_cmp, X.ev_in[c], 0);
     vxs_stats sc{};
     st = run_sort<W>(A + cs.off[c], cs.off[c + 1] - cs.off[c], xf, seed + (uint64_t)c * 0x9E3779B97F4A7C15ull,
-                     nullptr, 0, X.s_cmp, &sc);
+                     cws, cws_bytes, X.s_cmp, &sc);
     add_stats(acc, sc);
     if (trace) {
       cudaEvent_t ev;
@@ -1198,6 +1206,7 @@ vxs_status host_pipeline(PipeCtx& X, W* h, size_t n, int xf, uint64_t seed, int 
   if (B) cudaFreeAsync(B, X.s_cmp);
   if (small) cudaFreeAsync(small, X.s_cmp);
   if (Tb) cudaFreeAsync(Tb, X.s_cmp);
+  if (cws) cudaFreeAsync(cws, X.s_cmp);
   e = cudaStreamSynchronize(X.s_cmp);
   if (st == VXS_OK && e != cudaSuccess) st = cuda_fail(e, "pipeline sync");
   if (st == VXS_OK && thread_err[0] != cudaSuccess) st = cuda_fail(thread_err[0], "H2D");
