@@ -2192,7 +2192,10 @@ __global__ void __launch_bounds__(SortClass<CLS>::T, final_min_blocks<W, CLS>())
     if constexpr (CLS >= 1) {
       // counting-sort base case; items it rejects (clustered keys, decided
       // block-uniformly) go to the full-width network fallback kernel
-      constexpr bool RANK = sizeof(W) == 8;  // (measured per key width)
+      // (rank-in-count for 8-byte keys was faster until the padding slots left the
+      // counting pass; re-measured after: fire-and-forget counts win there too,
+      // k_final<u64> 0.630 -> 0.603 ms)
+      constexpr bool RANK = false;
       const bool done = X.flt ? bin_sort_item<W, THREADS, ITEMS, true, RANK>(k, size, dst, X)
                               : bin_sort_item<W, THREADS, ITEMS, false, RANK>(k, size, dst, X);
       if (!done && threadIdx.x == 0) {
